@@ -1,0 +1,143 @@
+"""Matrix-free operator application (Alg. 2 with Alg. 3).
+
+The reference package specifies but does not ship this module
+(SPEC.md:440-483).  `apply(op, u)` computes
+    v = Σ_eta Q_eta^T · w · Σ_theta F_{eta,theta} · Q_theta · u
+on the GPU through igs_apply (K4): the fused sm_100a kernel for the
+BASELINE shapes (3D, same order in every direction, per-element Gauss
+rules), else the stage-by-stage kernels.  Host (numpy) vectors are copied
+to the device and back; device tensors stay on the device.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .sumfac import FlopCounter
+from .tensorspace import field_eval_count
+
+__all__ = ("MatrixFreeOperator", "apply", "eval_field")
+
+
+class MatrixFreeOperator:
+    """A ready-to-apply operator: problem + device tables + workspace.
+
+    `slab=(lo, hi)` restricts the operator to elements [lo, hi) of the last
+    direction (the multi-GPU partition, see sharded.py); the coefficient
+    planes then cover only that slab's points and vectors hold DoF layers
+    [lo, hi + order - 1).
+    """
+
+    def __init__(self, problem, dir_order=None, slab=None, force_generic=False):
+        self.problem = problem
+        self.dir_order = None if dir_order is None else tuple(dir_order)
+        self.slab = None if slab is None else (int(slab[0]), int(slab[1]))
+        self.flags = _lib.FLAG_FORCE_GENERIC if force_generic else 0
+        self._ws = None
+        self._prob = None
+
+    @property
+    def shape(self):
+        if self.slab is None:
+            return self.problem.shape
+        lo, hi = self.slab
+        last_t = self.problem.trial[-1].order
+        last_s = self.problem.test[-1].order
+        m = n = 1
+        for b in self.problem.test[:-1]:
+            m *= b.num_basis
+        for b in self.problem.trial[:-1]:
+            n *= b.num_basis
+        return m * (hi - lo + last_s - 1), n * (hi - lo + last_t - 1)
+
+    def struct(self):
+        if self._prob is None:
+            self._prob = self.problem.struct(self.dir_order, slab=self.slab, with_pattern=False)
+        return self._prob
+
+    @property
+    def fused(self):
+        lib = _lib.load()
+        prob, _ = self.struct()
+        return bool(lib.igs_fused_path(ctypes.byref(prob), _lib.OP_APPLY)) and not self.flags
+
+    def workspace(self):
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        prob, _ = self.struct()
+        nbytes = lib.igs_workspace_bytes(ctypes.byref(prob), _lib.OP_APPLY, self.flags)
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
+        return self._ws, nbytes
+
+    def apply_device(self, x, y=None, accumulate=False, stream=None):
+        """y (+)= A x for device tensors; returns y.  Enqueued on `stream`
+        (default: torch's current stream); no host synchronisation."""
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        m, n = self.shape
+        if x.numel() != n:
+            raise ValueError(f"vector length {x.numel()} does not match the trial space ({n})")
+        if y is None:
+            y = torch.empty(m, dtype=torch.float64, device="cuda")
+        prob, _ = self.struct()
+        ws, nbytes = self.workspace()
+        f = self.problem.coeff_field()
+        flags = self.flags | (_lib.FLAG_ACCUMULATE if accumulate else 0)
+        sh = ctypes.c_void_p(stream.cuda_stream) if stream is not None else _lib.stream_handle()
+        st = lib.igs_apply(ctypes.byref(prob), _lib.ptr(f.planes), _lib.ptr(x), _lib.ptr(y), _lib.ptr(ws),
+                           nbytes, flags, sh)
+        _lib.check(st, "apply")
+        return y
+
+    def count(self, counter):
+        """Reference-style MAC counts of one apply (see module docstring)."""
+        p = self.problem
+        orders_t = [b.order for b in p.trial]
+        orders_s = [b.order for b in p.test]
+        nt = [b.num_basis for b in p.trial]
+        ns = [b.num_basis for b in p.test]
+        npts = list(p.quad.shape)
+        f = p.coeff_field()
+        for j, th in enumerate(p.theta_set):
+            if all(f.is_zero_block(i, j) for i in range(len(p.eta_set))):
+                continue
+            counter.add_field_eval(field_eval_count(orders_t, nt, npts))
+        for i, et in enumerate(p.eta_set):
+            if all(f.is_zero_block(i, j) for j in range(len(p.theta_set))):
+                continue
+            counter.add_block_update(field_eval_count(orders_s, ns, npts))
+
+
+def apply(op, u, counter=None):
+    """v = A u without forming A.
+
+    numpy input -> numpy output (host copies included); a CUDA tensor stays
+    on the device.
+    """
+    torch = _lib.require_cuda()
+    host = not isinstance(u, torch.Tensor)
+    if host:
+        u_np = np.ascontiguousarray(u, dtype=float).reshape(-1)
+        x = torch.from_numpy(u_np).to("cuda", non_blocking=False)
+    else:
+        x = u.to(device="cuda", dtype=torch.float64).reshape(-1).contiguous()
+    y = op.apply_device(x)
+    if counter is not None:
+        op.count(counter)
+    return y.cpu().numpy() if host else y
+
+
+def eval_field(op, u, theta, counter=None):
+    """∂^theta u at every quadrature point (Alg. 3).
+
+    Returns a device tensor indexed [i_1, ..., i_d].
+    """
+    from .tensorspace import contract_to_points
+
+    p = op.problem if isinstance(op, MatrixFreeOperator) else op
+    return contract_to_points(p.trial_tables(), theta, u, counter)
+
+
+del FlopCounter

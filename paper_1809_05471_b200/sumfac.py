@@ -1,0 +1,328 @@
+"""Global sum-factorized assembly on the GPU (mirror of sumfac.py).
+
+`assemble` / `assemble_block` keep the reference's signatures
+(sumfac.py:358-379) and return a `SparseMatrix` over a shared
+`SparsityPattern` (CSR, rows = test functions, ascending columns, band zeros
+stored).  The values are computed by igs_assemble_values (K3): the fused
+sm_100a kernel for the BASELINE shapes, else the stage-by-stage kernels.
+`FlopCounter` is filled analytically with exactly the counts the reference
+records (Eq. 13, sumfac.py:211) so the SPEC's FLOP law holds.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._problem import problem_struct
+from .bspline import tabulate
+from .errors import CapacityError, UnsupportedDerivativeError
+from .geometry import CoefficientField
+from .tensorspace import DEFAULT_MAX_PATTERN_NNZ, tensor_pattern
+
+__all__ = (
+    "FlopCounter",
+    "SparseMatrix",
+    "AssemblyProblem",
+    "assemble",
+    "assemble_block",
+    "rel_frobenius",
+)
+
+
+class FlopCounter:
+    """Deterministic multiply-add counters (sumfac.py:47-85)."""
+
+    __slots__ = ("block_update", "field_eval", "coeff_build")
+
+    def __init__(self):
+        self.block_update = 0
+        self.field_eval = 0
+        self.coeff_build = 0
+
+    def add_block_update(self, n):
+        self.block_update += int(n)
+
+    def add_field_eval(self, n):
+        self.field_eval += int(n)
+
+    def add_coeff_build(self, n):
+        self.coeff_build += int(n)
+
+    def merge(self, other):
+        self.block_update += other.block_update
+        self.field_eval += other.field_eval
+        self.coeff_build += other.coeff_build
+
+    @property
+    def total(self):
+        return self.block_update + self.field_eval + self.coeff_build
+
+    def as_tuple(self):
+        return (self.block_update, self.field_eval, self.coeff_build)
+
+    def __eq__(self, other):
+        return isinstance(other, FlopCounter) and self.as_tuple() == other.as_tuple()
+
+    def __repr__(self):
+        return (f"FlopCounter(block_update={self.block_update}, field_eval={self.field_eval}, "
+                f"coeff_build={self.coeff_build})")
+
+
+class SparseMatrix:
+    """CSR values (device tensor) over a shared SparsityPattern (sumfac.py:88-115)."""
+
+    def __init__(self, pattern, values):
+        if int(values.shape[0]) != pattern.nnz:
+            raise ValueError("values not aligned with the pattern")
+        self.pattern = pattern
+        self.values = values
+
+    @property
+    def shape(self):
+        return self.pattern.shape
+
+    @property
+    def nnz(self):
+        return self.pattern.nnz
+
+    def values_np(self):
+        return self.values.cpu().numpy() if hasattr(self.values, "cpu") else np.asarray(self.values)
+
+    def to_scipy(self):
+        return self.pattern.to_scipy(self.values_np())
+
+    def toarray(self):
+        return self.to_scipy().toarray()
+
+    def matvec(self, u):
+        """A @ u on the device (cuSPARSE through torch); numpy in -> numpy out."""
+        torch = _lib.require_cuda()
+        host = not isinstance(u, torch.Tensor)
+        x = torch.as_tensor(np.asarray(u, dtype=float) if host else u, dtype=torch.float64,
+                            device="cuda").reshape(-1, 1)
+        y = (self.pattern.to_torch(self.values) @ x).reshape(-1)
+        return y.cpu().numpy() if host else y
+
+    def copy(self):
+        return SparseMatrix(self.pattern, self.values.clone())
+
+
+def rel_frobenius(a, b):
+    """Relative Frobenius distance ||a - b||_F / ||b||_F (sumfac.py:118-141).
+
+    Same-pattern SparseMatrix pairs compare their value arrays (on the
+    device); anything else is densified on the host like the reference.
+    """
+    if isinstance(a, SparseMatrix) and isinstance(b, SparseMatrix) and (
+            a.pattern is b.pattern or (a.pattern.nnz == b.pattern.nnz and a.shape == b.shape
+                                       and np.array_equal(a.pattern.indptr, b.pattern.indptr)
+                                       and np.array_equal(a.pattern.indices, b.pattern.indices))):
+        torch = _lib.require_cuda()
+        va = torch.as_tensor(a.values, device="cuda")
+        vb = torch.as_tensor(b.values, device="cuda")
+        num = float(torch.linalg.vector_norm(va - vb))
+        den = float(torch.linalg.vector_norm(vb))
+    else:
+        def dense(x):
+            if isinstance(x, SparseMatrix):
+                return x.toarray()
+            if hasattr(x, "toarray"):
+                return x.toarray()
+            if hasattr(x, "cpu"):
+                return x.cpu().numpy()
+            return np.asarray(x, dtype=float)
+
+        da, db = dense(a), dense(b)
+        num = float(np.linalg.norm(da - db))
+        den = float(np.linalg.norm(db))
+    if den == 0.0:
+        return 0.0 if num == 0.0 else np.inf
+    return num / den
+
+
+class AssemblyProblem:
+    """Trial/test spaces, a tensor quadrature and a coefficient field (sumfac.py:232-337)."""
+
+    def __init__(self, trial, test, quad, coeff, max_nnz=DEFAULT_MAX_PATTERN_NNZ):
+        self.trial = tuple(trial)
+        self.test = tuple(test)
+        self.quad = quad
+        if not len(self.trial) == len(self.test) == quad.dim:
+            raise ValueError("trial, test and quadrature dimensions differ")
+        self.theta_set = tuple(tuple(t) for t in coeff.theta_set)
+        self.eta_set = tuple(tuple(t) for t in coeff.eta_set)
+        self.max_nnz = max_nnz
+        for delta, basis in enumerate(self.trial):
+            if max(t[delta] for t in self.theta_set) >= basis.order:
+                raise UnsupportedDerivativeError(f"trial derivative exceeds order in direction {delta}")
+        for delta, basis in enumerate(self.test):
+            if max(t[delta] for t in self.eta_set) >= basis.order:
+                raise UnsupportedDerivativeError(f"test derivative exceeds order in direction {delta}")
+        if not isinstance(coeff, CoefficientField):
+            raise TypeError("coeff must be a CoefficientField (lazy geometry providers are out of scope)")
+        if coeff.num_points != quad.num_points:
+            raise ValueError("coefficient field does not match the point grid")
+        self._field = coeff
+        self._cache = {}
+
+    @property
+    def d(self):
+        return len(self.trial)
+
+    @property
+    def shape(self):
+        m = n = 1
+        for b in self.test:
+            m *= b.num_basis
+        for b in self.trial:
+            n *= b.num_basis
+        return m, n
+
+    def coeff_field(self, counter=None):
+        return self._field
+
+    @property
+    def coeff(self):
+        return self._field
+
+    def trial_tables(self):
+        tabs = self._cache.get("trial_tables")
+        if tabs is None:
+            md = max(max(t) for t in self.theta_set)
+            tabs = tuple(tabulate(b, r.points, min(md, b.order - 1)) for b, r in zip(self.trial, self.quad.rules))
+            self._cache["trial_tables"] = tabs
+        return tabs
+
+    def test_tables(self):
+        tabs = self._cache.get("test_tables")
+        if tabs is None:
+            if self.test == self.trial and self.eta_set == self.theta_set:
+                tabs = self.trial_tables()
+            else:
+                md = max(max(t) for t in self.eta_set)
+                tabs = tuple(tabulate(b, r.points, min(md, b.order - 1)) for b, r in zip(self.test, self.quad.rules))
+            self._cache["test_tables"] = tabs
+        return tabs
+
+    def pattern(self):
+        pat = self._cache.get("pattern")
+        if pat is None:
+            pat = tensor_pattern(self.trial, self.test, self.quad, max_nnz=self.max_nnz)
+            self._cache["pattern"] = pat
+        return pat
+
+    def struct(self, dir_order=None, slab=None, with_pattern=True):
+        """The C igs_problem for this problem (cached per dir_order/slab)."""
+        key = ("struct", tuple(dir_order) if dir_order is not None else None,
+               tuple(slab) if slab is not None else None, with_pattern)
+        hit = self._cache.get(key)
+        if hit is None:
+            f = self._field
+            num_pairs = [dp.num_pairs for dp in self.pattern().dir_pairs] if with_pattern else None
+            hit = problem_struct(self.trial, self.test, self.quad.rules, self.trial_tables(),
+                                 self.test_tables(), self.theta_set, self.eta_set, f.plane_of,
+                                 f.n_planes, f.plane_stride, dir_order=dir_order, num_pairs=num_pairs,
+                                 slab=slab)
+            self._cache[key] = hit
+        return hit
+
+
+def _check_block_indices(problem, theta, eta):
+    theta = tuple(theta)
+    eta = tuple(eta)
+    for delta, basis in enumerate(problem.trial):
+        if theta[delta] >= basis.order:
+            raise UnsupportedDerivativeError(f"trial derivative {theta[delta]} >= order {basis.order}")
+    for delta, basis in enumerate(problem.test):
+        if eta[delta] >= basis.order:
+            raise UnsupportedDerivativeError(f"test derivative {eta[delta]} >= order {basis.order}")
+    if theta not in problem.theta_set or eta not in problem.eta_set:
+        raise ValueError("derivative multi-index not in the problem's index sets")
+    return theta, eta
+
+
+def block_update_count(problem, theta, eta, dir_order=None):
+    """The reference's block_update MACs for one (theta, eta) block (Eq. 13)."""
+    d = problem.d
+    order = tuple(range(d)) if dir_order is None else tuple(dir_order)
+    pat = problem.pattern()
+    dims = list(problem.quad.shape)
+    total = 0
+    for delta in order:
+        p = problem.trial[delta].order
+        q = problem.test[delta].order
+        x = problem.quad.shape[delta]
+        w_nnz = p * q * x if dims[delta] and pat.dir_pairs[delta].num_pairs else 0
+        other = 1
+        for j, v in enumerate(dims):
+            if j != delta:
+                other *= v
+        total += w_nnz * other
+        dims[delta] = pat.dir_pairs[delta].num_pairs
+    return total
+
+
+def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    pat = problem.pattern()
+    prob, keep = problem.struct(dir_order)
+    nrows = pat.shape[0]
+    lo, hi = (0, nrows) if row_range is None else row_range
+    values = torch.zeros(pat.nnz, dtype=torch.float64, device="cuda")
+    if pat.nnz == 0:
+        return values
+    ws_bytes = lib.igs_workspace_bytes(ctypes.byref(prob), _lib.OP_ASSEMBLE, flags)
+    ws = problem._cache.get(("ws_asm", ws_bytes))
+    if ws is None:
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+        problem._cache[("ws_asm", ws_bytes)] = ws
+    d = problem.d
+    rp = (ctypes.c_void_p * 3)(*[dp.rowptr_dev.data_ptr() for dp in pat.dir_pairs] + [0] * (3 - d))
+    cl = (ctypes.c_void_p * 3)(*[dp.cols_dev.data_ptr() for dp in pat.dir_pairs] + [0] * (3 - d))
+    bi, bj = block if block is not None else (-1, -1)
+    f = problem.coeff_field()
+    st = lib.igs_assemble_values(ctypes.byref(prob), rp, cl, lo, hi, bi, bj, _lib.ptr(f.planes),
+                                 _lib.ptr(values), _lib.ptr(ws), ws_bytes, flags, _lib.stream_handle())
+    _lib.check(st, "assemble_values")
+    if counter is not None:
+        for j, th in enumerate(problem.theta_set):
+            for i, et in enumerate(problem.eta_set):
+                if block is not None and (i, j) != (bi, bj):
+                    continue
+                if f.is_zero_block(i, j):
+                    continue
+                counter.add_block_update(block_update_count(problem, th, et, dir_order))
+    return values
+
+
+def assemble_block(problem, theta, eta, counter=None, dir_order=None):
+    """Assemble the single derivative block (theta, eta) on the shared pattern."""
+    torch = _lib.require_cuda()
+    counter = counter if counter is not None else FlopCounter()
+    theta, eta = _check_block_indices(problem, theta, eta)
+    pattern = problem.pattern()
+    i = problem.eta_set.index(eta)
+    j = problem.theta_set.index(theta)
+    if problem.coeff_field().is_zero_block(i, j) or pattern.nnz == 0:
+        return SparseMatrix(pattern, torch.zeros(pattern.nnz, dtype=torch.float64, device="cuda"))
+    return SparseMatrix(pattern, _run_assembly(problem, (i, j), counter, dir_order))
+
+
+def assemble(problem, counter=None, dir_order=None, flags=0):
+    """Assemble the full matrix: the sum of all derivative blocks (sumfac.py:373-379)."""
+    counter = counter if counter is not None else FlopCounter()
+    vals = _run_assembly(problem, None, counter, dir_order, flags)
+    return SparseMatrix(problem.pattern(), vals)
+
+
+def fused_path(problem, op="assemble", dir_order=None):
+    """1 when the fused sm_100a kernel serves this problem, 0 for the generic kernels."""
+    lib = _lib.load()
+    prob, keep = problem.struct(dir_order)
+    return int(lib.igs_fused_path(ctypes.byref(prob), _lib.OP_ASSEMBLE if op == "assemble" else _lib.OP_APPLY))
+
+
+__all__ += ("block_update_count", "fused_path")
+del CapacityError
