@@ -99,7 +99,9 @@ enum { IGS_OP_ASSEMBLE = 1, IGS_OP_APPLY = 2, IGS_OP_EVAL_FIELD = 3, IGS_OP_PATT
 enum {
   IGS_FLAG_DEFAULT = 0,
   IGS_FLAG_FORCE_GENERIC = 1,   /* use the stage-by-stage kernels even when a fused one applies */
-  IGS_FLAG_ACCUMULATE = 2       /* y += A x instead of y = A x (apply only)              */
+  IGS_FLAG_ACCUMULATE = 2,      /* y += A x instead of y = A x (apply only)              */
+  IGS_FLAG_KERNEL_ONLY = 4      /* measurement: run only the fused apply's main kernel
+                                   (partial sums left in the workspace, y untouched)    */
 };
 
 /* ---- diagnostics ---------------------------------------------------- */

@@ -34,7 +34,6 @@ SOURCES = [
     "synth.cu",
     "apply3d.cu",
     "assemble3d.cu",
-    "fused_stub.cu",
 ]
 
 

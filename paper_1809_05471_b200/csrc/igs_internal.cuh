@@ -112,6 +112,9 @@ __device__ __forceinline__ int64_t tensor_row_start(const TensorPat& t, int64_t 
   return rpm[0] * w[1] * w[2] + P[0] * rpm[1] * w[2] + P[0] * P[1] * rpm[2];
 }
 
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t n, int64_t v) {
   int64_t lo = 0, hi = n;
   while (lo < hi) {

@@ -69,10 +69,16 @@ class CoefficientField:
         self.plane_of = tuple(tuple(r) for r in plane_of)
         self.point_shape = tuple(point_shape)
         self._num_points = int(npts)
+        self.slab = None
 
     @classmethod
-    def from_planes(cls, theta_set, eta_set, planes, plane_of, point_shape):
-        """Wrap device planes [n_planes, npts] with an explicit plane map."""
+    def from_planes(cls, theta_set, eta_set, planes, plane_of, point_shape, slab=None):
+        """Wrap device planes [n_planes, npts] with an explicit plane map.
+
+        `slab=(lo, hi)`: the planes hold only the points of elements
+        [lo, hi) of the last direction (one rank's part of a slab-
+        partitioned apply, sharded.py); `point_shape` stays the full grid.
+        """
         torch = _lib.require_cuda()
         self = cls.__new__(cls)
         self.theta_set = tuple(tuple(int(v) for v in t) for t in theta_set)
@@ -85,6 +91,7 @@ class CoefficientField:
             raise ValueError("plane_of must be [len(eta_set)][len(theta_set)]")
         self.point_shape = tuple(point_shape)
         self._num_points = int(planes.shape[1])
+        self.slab = None if slab is None else (int(slab[0]), int(slab[1]))
         return self
 
     @property

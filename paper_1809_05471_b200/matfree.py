@@ -32,6 +32,8 @@ class MatrixFreeOperator:
     def __init__(self, problem, dir_order=None, slab=None, force_generic=False):
         self.problem = problem
         self.dir_order = None if dir_order is None else tuple(dir_order)
+        if slab is None:
+            slab = getattr(problem, "slab", None)
         self.slab = None if slab is None else (int(slab[0]), int(slab[1]))
         self.flags = _lib.FLAG_FORCE_GENERIC if force_generic else 0
         self._ws = None
@@ -71,9 +73,10 @@ class MatrixFreeOperator:
             self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device="cuda")
         return self._ws, nbytes
 
-    def apply_device(self, x, y=None, accumulate=False, stream=None):
+    def apply_device(self, x, y=None, accumulate=False, stream=None, kernel_only=False):
         """y (+)= A x for device tensors; returns y.  Enqueued on `stream`
-        (default: torch's current stream); no host synchronisation."""
+        (default: torch's current stream); no host synchronisation.
+        `kernel_only` (measurement) runs only the fused main kernel."""
         torch = _lib.require_cuda()
         lib = _lib.load()
         m, n = self.shape
@@ -84,7 +87,7 @@ class MatrixFreeOperator:
         prob, _ = self.struct()
         ws, nbytes = self.workspace()
         f = self.problem.coeff_field()
-        flags = self.flags | (_lib.FLAG_ACCUMULATE if accumulate else 0)
+        flags = self.flags | (_lib.FLAG_ACCUMULATE if accumulate else 0) | (4 if kernel_only else 0)
         sh = ctypes.c_void_p(stream.cuda_stream) if stream is not None else _lib.stream_handle()
         st = lib.igs_apply(ctypes.byref(prob), _lib.ptr(f.planes), _lib.ptr(x), _lib.ptr(y), _lib.ptr(ws),
                            nbytes, flags, sh)

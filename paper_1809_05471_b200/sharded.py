@@ -1,0 +1,115 @@
+"""Slab partition of the matrix-free apply along the last (slowest) direction.
+
+SURVEY §8(e): rank r owns elements [lo_r, hi_r) of the last direction and
+the DoF layers [lo_r, hi_r) (the last rank also the trailing order-1
+layers).  One apply is
+
+  1. ghost gather : x layers [hi_r, hi_r + p - 1) from rank r+1      (p2p)
+  2. local apply  : y_local over DoF layers [lo_r, hi_r + p - 1)     (K4 on the slab)
+  3. ghost reduce : trailing p-1 y layers added into rank r+1          (p2p)
+
+The exchanges are point-to-point sends/receives through torch.distributed
+(NCCL over NVLink on GPUs, gloo in the CPU tests), issued as one batched
+group per step.  Each message is (p-1)·N0·N1 doubles.  The assembly needs
+no communication (row blocks are independent) and is not handled here.
+"""
+
+import torch
+import torch.distributed as dist
+
+
+class SlabPartition:
+    """Balanced split of K elements (last direction) over `world` ranks."""
+
+    def __init__(self, num_elements, order, world):
+        if world > num_elements:
+            raise ValueError("more ranks than element layers")
+        self.K = int(num_elements)
+        self.p = int(order)
+        self.world = int(world)
+        base, rem = divmod(self.K, self.world)
+        self.bounds = []
+        lo = 0
+        for r in range(self.world):
+            hi = lo + base + (1 if r < rem else 0)
+            self.bounds.append((lo, hi))
+            lo = hi
+        for r in range(self.world - 1):
+            lo, hi = self.bounds[r + 1]
+            if hi - lo < self.p - 1 and r + 1 < self.world - 1:
+                raise ValueError("slabs must hold at least order-1 element layers")
+
+    def elements(self, r):
+        return self.bounds[r]
+
+    def own_layers(self, r):
+        """DoF layers owned by rank r (disjoint, covering K + p - 1)."""
+        lo, hi = self.bounds[r]
+        return (lo, hi + self.p - 1) if r == self.world - 1 else (lo, hi)
+
+    def local_layers(self, r):
+        """DoF layers touched by rank r's elements (own + ghost)."""
+        lo, hi = self.bounds[r]
+        return lo, hi + self.p - 1
+
+
+class ShardedApply:
+    """Runs one rank's part of a slab-partitioned apply.
+
+    compute(x_local, y_local) must write the slab's y (DoF layers
+    local_layers(rank)) from x on the same layers — e.g.
+    MatrixFreeOperator(problem, slab=...).apply_device, or the CPU oracle.
+    """
+
+    def __init__(self, part, rank, layer_size, compute, device, dtype=torch.float64, group=None):
+        self.part = part
+        self.rank = int(rank)
+        self.layer = int(layer_size)
+        self.compute = compute
+        self.group = group
+        lo, hi = part.local_layers(self.rank)
+        olo, ohi = part.own_layers(self.rank)
+        self.n_local = (hi - lo) * self.layer
+        self.n_own = (ohi - olo) * self.layer
+        self.n_ghost = self.n_local - self.n_own
+        self.x_local = torch.zeros(self.n_local, dtype=dtype, device=device)
+        self.y_local = torch.zeros(self.n_local, dtype=dtype, device=device)
+        self.halo_in = torch.zeros((part.p - 1) * self.layer, dtype=dtype, device=device)
+
+    def _exchange(self, send, recv):
+        ops = []
+        for buf, peer in send:
+            ops.append(dist.P2POp(dist.isend, buf, peer, group=self.group))
+        for buf, peer in recv:
+            ops.append(dist.P2POp(dist.irecv, buf, peer, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def apply(self, x_own, y_own=None):
+        """y_own = (A x) restricted to this rank's own DoF layers."""
+        r, W, g = self.rank, self.part.world, (self.part.p - 1) * self.layer
+        self.x_local[: self.n_own].copy_(x_own)
+        # 1. ghost gather: my first p-1 own layers go to r-1; r+1's come to me.
+        send, recv = [], []
+        if r > 0 and g:
+            send.append((self.x_local[:g].clone() if self.x_local.device.type == "cpu" else self.x_local[:g], r - 1))
+        if r < W - 1 and g:
+            recv.append((self.x_local[self.n_own:], r + 1))
+        self._exchange(send, recv)
+        # 2. local apply on the slab
+        self.compute(self.x_local, self.y_local)
+        # 3. ghost reduce: my trailing p-1 partial layers go to r+1.
+        send, recv = [], []
+        if r < W - 1 and g:
+            send.append((self.y_local[self.n_own:], r + 1))
+        if r > 0 and g:
+            recv.append((self.halo_in, r - 1))
+        self._exchange(send, recv)
+        out = self.y_local[: self.n_own]
+        if r > 0 and g:
+            out[:g] += self.halo_in
+        if y_own is not None:
+            y_own.copy_(out)
+            return y_own
+        return out

@@ -161,8 +161,18 @@ class AssemblyProblem:
                 raise UnsupportedDerivativeError(f"test derivative exceeds order in direction {delta}")
         if not isinstance(coeff, CoefficientField):
             raise TypeError("coeff must be a CoefficientField (lazy geometry providers are out of scope)")
-        if coeff.num_points != quad.num_points:
-            raise ValueError("coefficient field does not match the point grid")
+        slab = getattr(coeff, "slab", None)
+        if slab is None:
+            if coeff.num_points != quad.num_points:
+                raise ValueError("coefficient field does not match the point grid")
+        else:
+            rule = quad.rules[-1]
+            if rule.points_per_element <= 0:
+                raise ValueError("slab fields need a per-element rule in the last direction")
+            want = quad.num_points // rule.num_points * (slab[1] - slab[0]) * rule.points_per_element
+            if coeff.num_points != want:
+                raise ValueError("slab coefficient field does not match the slab's points")
+        self.slab = slab
         self._field = coeff
         self._cache = {}
 
@@ -266,6 +276,8 @@ def block_update_count(problem, theta, eta, dir_order=None):
 def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
     torch = _lib.require_cuda()
     lib = _lib.load()
+    if problem.slab is not None:
+        raise ValueError("assembly needs the coefficient field on the whole grid (got a slab field)")
     pat = problem.pattern()
     prob, keep = problem.struct(dir_order)
     nrows = pat.shape[0]

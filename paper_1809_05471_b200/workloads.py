@@ -77,13 +77,13 @@ def synthetic_planes(d, point_dims, kind, seed=0, z_range=None, out=None):
     return out
 
 
-def field_from_planes(d, kind, planes, point_shape):
+def field_from_planes(d, kind, planes, point_shape, slab=None):
     torch = _lib.require_cuda()
     pm, npl = plane_map(d, kind)
     if not isinstance(planes, torch.Tensor):
         planes = torch.as_tensor(np.ascontiguousarray(planes), dtype=torch.float64, device="cuda")
     ths = first_order_derivative_set(d)
-    return CoefficientField.from_planes(ths, ths, planes, pm, point_shape)
+    return CoefficientField.from_planes(ths, ths, planes, pm, point_shape, slab=slab)
 
 
 def make_problem(d, p, K, kind, seed=0, planes=None, max_nnz=1 << 62, k=None):
