@@ -97,49 +97,68 @@ struct ApplyArgs {
   int64_t box;                // doubles per box
 };
 
+// fp64 tensor-core MMA (DMMA.8x8x4 on sm_100a): D(8x8) += A(8x4) · B(4x8).
+// Fragments (lane = 4·g + m): A[g][m], B[m][g], D[g][2m], D[g][2m+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Bulk L2 prefetch (cp.async.bulk.prefetch.L2): keeps the coefficient stream
+// flowing from HBM while the CTA is in its shared-memory-only phases.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
 struct Cfg {
+  static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
+  static constexpr int NT = 256, NW = NT / 32;
   static constexpr int FX = EX + P - 1, FY = EY + P - 1;
-  static constexpr int FXP = FX;             // row pitch of [n1][n0] arrays
+  static_assert(EX + 7 <= 16, "x footprint must fit two 8-column MMA tiles");
+  static constexpr int RP = 20;               // row pitch (16 used columns, bank-spread)
+  static constexpr int FYP = EY + 8;          // rows incl. MMA padding
   static constexpr int TX = EX * Q, TY = EY * Q;
-  static constexpr int NT = TY * EX;         // one (line, element) task per thread
-  static constexpr int NA = STIFF ? 2 : 1;   // z variants carried (val, der)
-  static constexpr int NV = STIFF ? 3 : 1;   // (y,z) variants carried: 00, 10, 01
-  static constexpr int XR = P * FY * FXP;
-  static constexpr int AA = NA * FY * FXP;
-  static constexpr int CC = NV * TY * FXP;   // C, then R (aliased)
-  static constexpr int RP = NV * TY * EX * P;
-  static constexpr int SS = NA * FY * FXP;
-  static constexpr int YR = P * FY * FXP;
-  static constexpr int TBX = EX * 2 * Q * P;
-  static constexpr int TBY = EY * 2 * Q * P;
-  static constexpr int TBZ = 2 * Q * P;
-  static constexpr int WW = TX + TY + Q;
-  static constexpr int TOTAL = XR + AA + CC + RP + SS + YR + TBX + TBY + TBZ + WW;
+  static_assert(TY % 8 == 0, "lines come in MMA groups of 8");
+  static constexpr int TYP = TY + 8;          // lines incl. padding read by Y^T
+  static constexpr int NLG = TY / 8;          // line groups of the X phase
+  static constexpr int NA = STIFF ? 2 : 1;    // z variants: value, z-derivative
+  static constexpr int NV = STIFF ? 3 : 1;    // (y, z) variants: 00, 10, 01
+  static constexpr int LXR = FYP * RP;        // one [n1][n0] plane
+  static constexpr int XR = P * LXR;          // x ring (P DoF layers)
+  static constexpr int AQ = NA * LXR;         // A for the current q2
+  static constexpr int CQ = NV * TYP * RP;    // C for the current q2, then R
+  static constexpr int RPT = NV * 8 * EX * TY;  // X^T partials [v][j][ex][line]
+  static constexpr int SQ = NA * LXR;         // S for the current q2
+  static constexpr int YR = P * LXR;          // y ring
+  static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 128;  // [e][v][q8][j8]
+  static constexpr int WW = TX + TY + 8;
+  static constexpr int TOTAL = XR + AQ + CQ + RPT + SQ + YR + TBX + TBY + TBZ + WW;
   static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double);
 };
 
 template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
-__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, MASS, STIFF>::NT)
-    apply3d_kernel(const ApplyArgs a) {
+__global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
   using C = Cfg<P, Q, EX, EY, MASS, STIFF>;
-  constexpr int FX = C::FX, FY = C::FY, FXP = C::FXP, TX = C::TX, TY = C::TY, NT = C::NT;
-  constexpr int NA = C::NA, NV = C::NV;
+  constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY, TYP = C::TYP;
+  constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR;
   extern __shared__ double sm[];
-  double* Xr = sm;                 // [P][FY][FXP]
-  double* Aa = Xr + C::XR;         // [NA][FY][FXP]
-  double* Cc = Aa + C::AA;         // [NV][TY][FXP]   (R aliases it)
-  double* Rp = Cc + C::CC;         // [NV][TY][EX][P]
-  double* Ss = Rp + C::RP;         // [NA][FY][FXP]
-  double* Yr = Ss + C::SS;         // [P][FY][FXP]
-  double* Tx = Yr + C::YR;         // [EX][2][Q][P]
-  double* Ty = Tx + C::TBX;        // [EY][2][Q][P]
-  double* Tz = Ty + C::TBY;        // [2][Q][P]
-  double* Wx = Tz + C::TBZ;        // [TX]
-  double* Wy = Wx + TX;            // [TY]
-  double* Wz = Wy + TY;            // [Q]
+  double* Xr = sm;              // [P][FYP][RP]
+  double* Aq = Xr + C::XR;      // [NA][FYP][RP]
+  double* Cq = Aq + C::AQ;      // [NV][TYP][RP]   (R aliases it)
+  double* Rp = Cq + C::CQ;      // [NV][8][EX][TY]
+  double* Sq = Rp + C::RPT;     // [NA][FYP][RP]
+  double* Yr = Sq + C::SQ;      // [P][FYP][RP]
+  double* Tx = Yr + C::YR;      // [EX][2][8][8]
+  double* Ty = Tx + C::TBX;     // [EY][2][8][8]
+  double* Tz = Ty + C::TBY;     // [2][8][8]
+  double* Wx = Tz + C::TBZ;     // [TX]
+  double* Wy = Wx + TX;         // [TY]
+  double* Wz = Wy + TY;         // [8]
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, m = lane & 3;  // MMA fragment coordinates
   const int item = blockIdx.x;
   const int tx = item % a.ntx;
   const int ty = (item / a.ntx) % a.nty;
@@ -149,235 +168,285 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, MASS, STIFF>::NT)
   const int z1 = min(a.K2, z0 + a.ez);
   double* box = a.scratch + (int64_t)item * a.box;
 
-  // ---- prologue: x/y tables + weights of the tile, zeroed y ring ------------
-  for (int i = tid; i < C::TBX; i += NT) {
+  // ---- prologue ---------------------------------------------------------------
+  for (int i = tid; i < C::TOTAL; i += NT) sm[i] = 0.0;  // all MMA padding is zero
+  __syncthreads();
+  for (int i = tid; i < EX * 2 * Q * P; i += NT) {
     int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
     int ge = ex0 + e;
-    Tx[i] = ge < a.K0 ? a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ge * Q + q] : 0.0;
+    if (ge < a.K0)
+      Tx[((e * 2 + v) * 8 + q) * 8 + j] = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ge * Q + q];
   }
-  for (int i = tid; i < C::TBY; i += NT) {
+  for (int i = tid; i < EY * 2 * Q * P; i += NT) {
     int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
     int ge = ey0 + e;
-    Ty[i] = ge < a.K1 ? a.vals[1][((int64_t)v * P + j) * a.xtab[1] + (int64_t)ge * Q + q] : 0.0;
+    if (ge < a.K1)
+      Ty[((e * 2 + v) * 8 + q) * 8 + j] = a.vals[1][((int64_t)v * P + j) * a.xtab[1] + (int64_t)ge * Q + q];
   }
   for (int i = tid; i < TX; i += NT) {
-    int64_t g = (int64_t)ex0 * Q + i;
-    Wx[i] = g < a.X0 ? a.wts[0][g] : 0.0;
+    int64_t gg = (int64_t)ex0 * Q + i;
+    if (gg < a.X0) Wx[i] = a.wts[0][gg];
   }
   for (int i = tid; i < TY; i += NT) {
-    int64_t g = (int64_t)ey0 * Q + i;
-    Wy[i] = g < a.X1 ? a.wts[1][g] : 0.0;
+    int64_t gg = (int64_t)ey0 * Q + i;
+    if (gg < a.X1) Wy[i] = a.wts[1][gg];
   }
-  for (int i = tid; i < C::YR; i += NT) Yr[i] = 0.0;
-
   auto load_layer = [&](int n2) {
-    double* dst = Xr + (n2 % P) * FY * FXP;
+    double* dst = Xr + (n2 % P) * LXR;
     for (int i = tid; i < FY * FX; i += NT) {
       int n0 = i % FX, n1 = i / FX;
       int64_t g0 = (int64_t)ex0 + n0, g1 = (int64_t)ey0 + n1;
       double v = 0.0;
       if (g0 < a.N0 && g1 < a.N1 && n2 < a.N2) v = __ldg(a.x + ((int64_t)n2 * a.N1 + g1) * a.N0 + g0);
-      dst[n1 * FXP + n0] = v;
+      dst[n1 * RP + n0] = v;
     }
   };
   for (int l = 0; l < P; ++l) load_layer(z0 + l);
 
-  // Line task of this thread in the X phase: (line q1, element ex).
-  const int t_q1 = tid / EX, t_ex = tid % EX;
-  const bool t_valid = (ex0 + t_ex) < a.K0 && (ey0 + t_q1 / Q) < a.K1;
-
   const double* Fc = MASS ? a.planes + (int64_t)a.pl_c * a.pstride : nullptr;
-  const double* Fa00 = STIFF ? a.planes + (int64_t)a.pl_a[0][0] * a.pstride : nullptr;
-  const double* Fa11 = STIFF ? a.planes + (int64_t)a.pl_a[1][1] * a.pstride : nullptr;
-  const double* Fa22 = STIFF ? a.planes + (int64_t)a.pl_a[2][2] * a.pstride : nullptr;
-  const double* Fa01 = STIFF ? a.planes + (int64_t)a.pl_a[0][1] * a.pstride : nullptr;
-  const double* Fa02 = STIFF ? a.planes + (int64_t)a.pl_a[0][2] * a.pstride : nullptr;
-  const double* Fa12 = STIFF ? a.planes + (int64_t)a.pl_a[1][2] * a.pstride : nullptr;
+  const double* F00 = STIFF ? a.planes + (int64_t)a.pl_a[0][0] * a.pstride : nullptr;
+  const double* F11 = STIFF ? a.planes + (int64_t)a.pl_a[1][1] * a.pstride : nullptr;
+  const double* F22 = STIFF ? a.planes + (int64_t)a.pl_a[2][2] * a.pstride : nullptr;
+  const double* F01 = STIFF ? a.planes + (int64_t)a.pl_a[0][1] * a.pstride : nullptr;
+  const double* F02 = STIFF ? a.planes + (int64_t)a.pl_a[0][2] * a.pstride : nullptr;
+  const double* F12 = STIFF ? a.planes + (int64_t)a.pl_a[1][2] * a.pstride : nullptr;
+  const double* Fpl[7] = {Fc, F00, F11, F22, F01, F02, F12};
+
+  // L2 prefetch of the coefficient rows of slab-local point layer zq.
+  const int nvalid_el_x = min(EX, a.K0 - ex0), nvalid_el_y = min(EY, a.K1 - ey0);
+  auto prefetch_layer = [&](int64_t zq) {
+    constexpr int NPL = 7;
+    const int rows = nvalid_el_y * Q;
+    const unsigned bytes = (unsigned)(nvalid_el_x * Q * sizeof(double));
+    for (int i = tid; i < NPL * rows; i += NT) {
+      int pl = i / rows, line = i % rows;
+      if (!Fpl[pl]) continue;
+      const double* p = Fpl[pl] + (zq * a.X1 + (int64_t)ey0 * Q + line) * a.X0 + (int64_t)ex0 * Q;
+      if (((uintptr_t)p & 15) == 0 && (bytes & 15) == 0) prefetch_l2(p, bytes);
+    }
+  };
+  const int64_t zq_end = (int64_t)z1 * Q;
+  prefetch_layer((int64_t)z0 * Q);
+  if (Q > 1 || z0 + 1 < z1) prefetch_layer((int64_t)z0 * Q + 1);
+
+  // Z^T of point layer q2 of the current element into the y ring (same item
+  // mapping as the Z phase, so each (n1, n0) is owned by one thread).
+  auto zt_item = [&](int e2, int q2, int i) {
+    int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
+    double s0 = Sq[o];
+    double s1 = STIFF ? Sq[LXR + o] : 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      double* yr = Yr + ((e2 + j) % P) * LXR + o;
+      double v = fma(Tz[(0 * 8 + q2) * 8 + j], s0, *yr);
+      if (STIFF) v = fma(Tz[(1 * 8 + q2) * 8 + j], s1, v);
+      *yr = v;
+    }
+  };
 
   for (int e2 = z0; e2 < z1; ++e2) {
-    // z tables and weights of this element layer
     const int gz = e2 + a.z_el_off;
-    for (int i = tid; i < C::TBZ; i += NT) {
+    for (int i = tid; i < 2 * Q * P; i += NT) {
       int j = i % P, q = (i / P) % Q, v = i / (P * Q);
-      Tz[i] = a.vals[2][((int64_t)v * P + j) * a.xtab[2] + (int64_t)gz * Q + q];
+      Tz[(v * 8 + q) * 8 + j] = a.vals[2][((int64_t)v * P + j) * a.xtab[2] + (int64_t)gz * Q + q];
     }
     for (int i = tid; i < Q; i += NT) Wz[i] = a.wts[2][(int64_t)gz * Q + i];
     __syncthreads();
 
     for (int q2 = 0; q2 < Q; ++q2) {
-      // ---- Z: contract the P active x layers to point layer q2 -------------
+      const int64_t zq = (int64_t)e2 * Q + q2;  // slab-local point layer
+      // ---- Z^T(q2-1) + Z(q2) + clear S ---------------------------------------
       for (int i = tid; i < FY * FX; i += NT) {
-        int n0 = i % FX, n1 = i / FX;
+        if (q2 > 0) zt_item(e2, q2 - 1, i);
+        int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
         for (int j = 0; j < P; ++j) {
-          double xv = Xr[((e2 + j) % P) * FY * FXP + n1 * FXP + n0];
-          a0 = fma(Tz[(0 * Q + q2) * P + j], xv, a0);
-          if (STIFF) a1 = fma(Tz[(1 * Q + q2) * P + j], xv, a1);
+          double xv = Xr[((e2 + j) % P) * LXR + o];
+          a0 = fma(Tz[(0 * 8 + q2) * 8 + j], xv, a0);
+          if (STIFF) a1 = fma(Tz[(1 * 8 + q2) * 8 + j], xv, a1);
         }
-        Aa[n1 * FXP + n0] = a0;
-        if (STIFF) Aa[FY * FXP + n1 * FXP + n0] = a1;
-      }
-      __syncthreads();
-      // ---- Y: contract y functions to y points -----------------------------
-      for (int i = tid; i < TY * FX; i += NT) {
-        int n0 = i % FX, q1 = i / FX;
-        int ey = q1 / Q, ql = q1 % Q;
-        const double* T0 = Ty + ((ey * 2 + 0) * Q + ql) * P;
-        const double* T1 = Ty + ((ey * 2 + 1) * Q + ql) * P;
-        double c00 = 0.0, c10 = 0.0, c01 = 0.0;
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          double a0 = Aa[(ey + j) * FXP + n0];
-          c00 = fma(T0[j], a0, c00);
-          if (STIFF) {
-            c10 = fma(T1[j], a0, c10);
-            c01 = fma(T0[j], Aa[FY * FXP + (ey + j) * FXP + n0], c01);
-          }
-        }
-        Cc[q1 * FXP + n0] = c00;
+        Aq[o] = a0;
+        Sq[o] = 0.0;
         if (STIFF) {
-          Cc[TY * FXP + q1 * FXP + n0] = c10;
-          Cc[2 * TY * FXP + q1 * FXP + n0] = c01;
+          Aq[LXR + o] = a1;
+          Sq[LXR + o] = 0.0;
         }
       }
+      if (zq + 2 < zq_end) prefetch_layer(zq + 2);
       __syncthreads();
-      // ---- X + pointwise + X^T partials (one line segment per thread) -------
-      {
-        double p00[P], p10[P], p01[P];
+
+      // ---- Y (DMMA): C_vw[q1][n0] = Σ_j By_w[q1][j] · A_v[ey+j][n0] ----------
+      for (int t = warp; t < EY * 2; t += NW) {
+        const int ey = t >> 1, nt = t & 1;
+        double c00[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0};
 #pragma unroll
-        for (int j = 0; j < P; ++j) p00[j] = p10[j] = p01[j] = 0.0;
-        if (t_valid) {
-          double c00[P], c10[P], c01[P];
-#pragma unroll
-          for (int j = 0; j < P; ++j) {
-            c00[j] = Cc[t_q1 * FXP + t_ex + j];
-            if (STIFF) {
-              c10[j] = Cc[TY * FXP + t_q1 * FXP + t_ex + j];
-              c01[j] = Cc[2 * TY * FXP + t_q1 * FXP + t_ex + j];
-            }
-          }
-          const int64_t zq = (int64_t)(e2 - 0) * Q + q2;  // slab-local point layer
-          const int64_t fo = (zq * a.X1 + (int64_t)ey0 * Q + t_q1) * a.X0 + (int64_t)(ex0 + t_ex) * Q;
-          const double wyz = Wz[q2] * Wy[t_q1];
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const double* T0 = Tx + ((t_ex * 2 + 0) * Q + q) * P;
-            const double* T1 = Tx + ((t_ex * 2 + 1) * Q + q) * P;
-            double u = 0.0, ux = 0.0, uy = 0.0, uz = 0.0;
-#pragma unroll
-            for (int j = 0; j < P; ++j) {
-              double b0 = T0[j];
-              if (MASS) u = fma(b0, c00[j], u);
-              if (STIFF) {
-                ux = fma(T1[j], c00[j], ux);
-                uy = fma(b0, c10[j], uy);
-                uz = fma(b0, c01[j], uz);
-              }
-            }
-            const double w = wyz * Wx[t_ex * Q + q];
-            double g0 = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-            if (MASS) g0 = w * (__ldg(Fc + fo + q) * u);
-            if (STIFF) {
-              double f00 = __ldg(Fa00 + fo + q), f11 = __ldg(Fa11 + fo + q), f22 = __ldg(Fa22 + fo + q);
-              double f01 = __ldg(Fa01 + fo + q), f02 = __ldg(Fa02 + fo + q), f12 = __ldg(Fa12 + fo + q);
-              gx = w * fma(f00, ux, fma(f01, uy, f02 * uz));
-              gy = w * fma(f01, ux, fma(f11, uy, f12 * uz));
-              gz = w * fma(f02, ux, fma(f12, uy, f22 * uz));
-            }
-#pragma unroll
-            for (int j = 0; j < P; ++j) {
-              double b0 = T0[j];
-              if (STIFF) {
-                p00[j] = fma(T1[j], gx, p00[j]);
-                p10[j] = fma(b0, gy, p10[j]);
-                p01[j] = fma(b0, gz, p01[j]);
-              }
-              if (MASS) p00[j] = fma(b0, g0, p00[j]);
-            }
-          }
-        }
-        double* r = Rp + (t_q1 * EX + t_ex) * P;
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          r[j] = p00[j];
+        for (int s = 0; s < 2; ++s) {
+          const int j = m + 4 * s;
+          const double t0 = Ty[((ey * 2 + 0) * 8 + g) * 8 + j];
+          const double b0 = Aq[(ey + j) * RP + nt * 8 + g];
+          dmma(c00[0], c00[1], t0, b0);
           if (STIFF) {
-            r[TY * EX * P + j] = p10[j];
-            r[2 * TY * EX * P + j] = p01[j];
+            const double t1 = Ty[((ey * 2 + 1) * 8 + g) * 8 + j];
+            const double b1 = Aq[LXR + (ey + j) * RP + nt * 8 + g];
+            dmma(c10[0], c10[1], t1, b0);
+            dmma(c01[0], c01[1], t0, b1);
+          }
+        }
+        if (g < Q) {
+          const int o = (ey * Q + g) * RP + nt * 8 + 2 * m;
+          Cq[o] = c00[0];
+          Cq[o + 1] = c00[1];
+          if (STIFF) {
+            Cq[TYP * RP + o] = c10[0];
+            Cq[TYP * RP + o + 1] = c10[1];
+            Cq[2 * TYP * RP + o] = c01[0];
+            Cq[2 * TYP * RP + o + 1] = c01[1];
           }
         }
       }
       __syncthreads();
-      // ---- X^T: overlap-add the element partials into R (aliases C) --------
+
+      // ---- X (DMMA) + pointwise + X^T (DMMA): task = (element ex, 8 lines) ----
+      for (int t = warp; t < EX * C::NLG; t += NW) {
+        const int ex = t % EX, lg = t / EX;
+        const int line = lg * 8 + g;  // A-fragment / D row
+        const int gex = ex0 + ex;
+        // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q];
+        // D column n holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two
+        // D values are points q = m and q = m + 4 -- exactly the A-fragment
+        // columns of the transposed product below (no shuffles needed).
+        const int qn = (g >> 1) + 4 * (g & 1);
+        double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int j = m + 4 * s;
+          const double b0 = Tx[((ex * 2 + 0) * 8 + qn) * 8 + j];
+          const double c0 = Cq[line * RP + ex + j];
+          if (MASS) dmma(u[0], u[1], c0, b0);
+          if (STIFF) {
+            const double b1 = Tx[((ex * 2 + 1) * 8 + qn) * 8 + j];
+            const double c1 = Cq[TYP * RP + line * RP + ex + j];
+            const double c2 = Cq[2 * TYP * RP + line * RP + ex + j];
+            dmma(ux[0], ux[1], c0, b1);
+            dmma(uy[0], uy[1], c1, b0);
+            dmma(uz[0], uz[1], c2, b0);
+          }
+        }
+        // pointwise: g = w · F(x) · (u, ∇u) at points (line, m) and (line, m+4)
+        const bool row_ok = gex < a.K0 && (ey0 + line / Q) < a.K1;
+        double g0[2], gx[2], gy[2], gz[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int q = m + 4 * c;
+          g0[c] = gx[c] = gy[c] = gz[c] = 0.0;
+          if (q < Q && row_ok) {
+            const int64_t fo = (zq * a.X1 + (int64_t)ey0 * Q + line) * a.X0 + (int64_t)gex * Q + q;
+            const double w = Wz[q2] * Wy[line] * Wx[ex * Q + q];
+            if (MASS) g0[c] = w * (__ldg(Fc + fo) * u[c]);
+            if (STIFF) {
+              const double f00 = __ldg(F00 + fo), f11 = __ldg(F11 + fo), f22 = __ldg(F22 + fo);
+              const double f01 = __ldg(F01 + fo), f02 = __ldg(F02 + fo), f12 = __ldg(F12 + fo);
+              gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
+              gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
+              gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
+            }
+          }
+        }
+        // transpose: R^T[line][j] = Σ_q g^T[line][q] · B[q][j]
+        double r00[2] = {0.0, 0.0}, r10[2] = {0.0, 0.0}, r01[2] = {0.0, 0.0};
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int q = m + 4 * s;
+          const double b0 = Tx[((ex * 2 + 0) * 8 + q) * 8 + g];
+          if (MASS) dmma(r00[0], r00[1], g0[s], b0);
+          if (STIFF) {
+            const double b1 = Tx[((ex * 2 + 1) * 8 + q) * 8 + g];
+            dmma(r00[0], r00[1], gx[s], b1);
+            dmma(r10[0], r10[1], gy[s], b0);
+            dmma(r01[0], r01[1], gz[s], b0);
+          }
+        }
+        // partials Rp[v][j][ex][line] with j = 2m + c
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int o = ((2 * m + c) * EX + ex) * TY + line;
+          Rp[o] = r00[c];
+          if (STIFF) {
+            Rp[8 * EX * TY + o] = r10[c];
+            Rp[2 * 8 * EX * TY + o] = r01[c];
+          }
+        }
+      }
+      __syncthreads();
+
+      // ---- X^T overlap-add: R_v[line][n0] = Σ_s partial(ex = n0 - s, j = s) -----
       for (int i = tid; i < TY * FX; i += NT) {
-        int n0 = i % FX, q1 = i / FX;
-        int s_lo = n0 - (EX - 1) > 0 ? n0 - (EX - 1) : 0;
-        int s_hi = n0 < P - 1 ? n0 : P - 1;
+        const int line = i % TY, n0 = i / TY;
+        const int s_lo = n0 - (EX - 1) > 0 ? n0 - (EX - 1) : 0;
+        const int s_hi = n0 < 7 ? n0 : 7;
         double r00 = 0.0, r10 = 0.0, r01 = 0.0;
         for (int s = s_lo; s <= s_hi; ++s) {
-          int o = (q1 * EX + (n0 - s)) * P + s;
+          const int o = (s * EX + (n0 - s)) * TY + line;
           r00 += Rp[o];
           if (STIFF) {
-            r10 += Rp[TY * EX * P + o];
-            r01 += Rp[2 * TY * EX * P + o];
+            r10 += Rp[8 * EX * TY + o];
+            r01 += Rp[2 * 8 * EX * TY + o];
           }
         }
-        Cc[q1 * FXP + n0] = r00;
+        Cq[line * RP + n0] = r00;
         if (STIFF) {
-          Cc[TY * FXP + q1 * FXP + n0] = r10;
-          Cc[2 * TY * FXP + q1 * FXP + n0] = r01;
+          Cq[TYP * RP + line * RP + n0] = r10;
+          Cq[2 * TYP * RP + line * RP + n0] = r01;
         }
       }
       __syncthreads();
-      // ---- Y^T + Z^T: test back in y, then accumulate into the y ring -------
-      for (int i = tid; i < FY * FX; i += NT) {
-        int n0 = i % FX, n1 = i / FX;
-        int e_lo = n1 - (P - 1) > 0 ? n1 - (P - 1) : 0;
-        int e_hi = n1 < EY - 1 ? n1 : EY - 1;
-        double s0 = 0.0, s1 = 0.0;
-        for (int ey = e_lo; ey <= e_hi; ++ey) {
-          int j = n1 - ey;
+
+      // ---- Y^T (DMMA): S_v[ey+j][n0] += Σ_q By[q][j] · R[ey*Q+q][n0] ----------
+      for (int t = warp; t < C::NA * 2; t += NW) {
+        const int grp = t >> 1, nt = t & 1;
+        for (int ey = 0; ey < EY; ++ey) {
+          double d[2] = {0.0, 0.0};
 #pragma unroll
-          for (int ql = 0; ql < Q; ++ql) {
-            int q1 = ey * Q + ql;
-            double b0 = Ty[((ey * 2 + 0) * Q + ql) * P + j];
-            s0 = fma(b0, Cc[q1 * FXP + n0], s0);
-            if (STIFF) {
-              s0 = fma(Ty[((ey * 2 + 1) * Q + ql) * P + j], Cc[TY * FXP + q1 * FXP + n0], s0);
-              s1 = fma(b0, Cc[2 * TY * FXP + q1 * FXP + n0], s1);
+          for (int s = 0; s < 2; ++s) {
+            const int q = m + 4 * s;
+            const int line = ey * Q + q;  // < TYP (padding rows are zero)
+            const double t0 = Ty[((ey * 2 + 0) * 8 + q) * 8 + g];
+            const int o = line * RP + nt * 8 + g;
+            if (grp == 0) {
+              dmma(d[0], d[1], t0, Cq[o]);
+              if (STIFF) dmma(d[0], d[1], Ty[((ey * 2 + 1) * 8 + q) * 8 + g], Cq[TYP * RP + o]);
+            } else {
+              dmma(d[0], d[1], t0, Cq[2 * TYP * RP + o]);
             }
           }
-        }
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          double* yr = Yr + ((e2 + j) % P) * FY * FXP + n1 * FXP + n0;
-          double v = fma(Tz[(0 * Q + q2) * P + j], s0, *yr);
-          if (STIFF) v = fma(Tz[(1 * Q + q2) * P + j], s1, v);
-          *yr = v;
+          double* srow = Sq + grp * LXR + (ey + g) * RP + nt * 8 + 2 * m;
+          srow[0] += d[0];
+          srow[1] += d[1];
+          __syncwarp();
         }
       }
       __syncthreads();
     }
-    // ---- DoF layer e2 is complete for this chunk: flush, recycle the slots -
-    {
-      double* yr = Yr + (e2 % P) * FY * FXP;
-      double* dst = box + (int64_t)(e2 - z0) * FY * FX;
-      for (int i = tid; i < FY * FX; i += NT) {
-        int n0 = i % FX, n1 = i / FX;
-        dst[i] = yr[n1 * FXP + n0];
-        yr[n1 * FXP + n0] = 0.0;
-      }
+    // last Z^T of the element, flush DoF layer e2 (complete for this chunk)
+    for (int i = tid; i < FY * FX; i += NT) {
+      zt_item(e2, Q - 1, i);
+      int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
+      double* yr = Yr + (e2 % P) * LXR + o;
+      box[(int64_t)(e2 - z0) * FY * FX + i] = *yr;
+      *yr = 0.0;
     }
+    __syncthreads();
     load_layer(e2 + P);
     __syncthreads();
   }
-  // trailing P-1 layers [z1, z1 + P - 1)
+  // trailing P-1 DoF layers [z1, z1 + P - 1)
   for (int l = z1; l < z1 + P - 1; ++l) {
-    double* yr = Yr + (l % P) * FY * FXP;
+    const double* yr = Yr + (l % P) * LXR;
     double* dst = box + (int64_t)(l - z0) * FY * FX;
     for (int i = tid; i < FY * FX; i += NT) {
       int n0 = i % FX, n1 = i / FX;
-      dst[i] = yr[n1 * FXP + n0];
+      dst[i] = yr[n1 * RP + n0];
     }
   }
 }
@@ -440,18 +509,17 @@ Launch make_launch() {
   return Launch{EX, EY, C::NT, C::SMEM, &apply3d_kernel<P, Q, EX, EY, MASS, STIFF>};
 }
 
-// Tile shapes per order: NT = EX·EY·Q threads, shared memory < 113 KB so
-// two CTAs fit on an SM where possible.
+// Tile shapes per order (256 threads; EY·Q lines must be a multiple of 8).
 template <bool MASS, bool STIFF>
 bool pick(int P, int Q, Launch* L) {
   if (P != Q) return false;
   switch (P) {
-    case 2: *L = make_launch<2, 2, 8, 16, MASS, STIFF>(); return true;
+    case 2: *L = make_launch<2, 2, 8, 4, MASS, STIFF>(); return true;
     case 3: *L = make_launch<3, 3, 8, 8, MASS, STIFF>(); return true;
-    case 4: *L = make_launch<4, 4, 8, 8, MASS, STIFF>(); return true;
-    case 5: *L = make_launch<5, 5, 8, 6, MASS, STIFF>(); return true;
-    case 6: *L = make_launch<6, 6, 8, 8, MASS, STIFF>(); return true;
-    case 7: *L = make_launch<7, 7, 8, 4, MASS, STIFF>(); return true;
+    case 4: *L = make_launch<4, 4, 8, 4, MASS, STIFF>(); return true;
+    case 5: *L = make_launch<5, 5, 8, 8, MASS, STIFF>(); return true;
+    case 6: *L = make_launch<6, 6, 8, 4, MASS, STIFF>(); return true;
+    case 7: *L = make_launch<7, 7, 8, 8, MASS, STIFF>(); return true;
     case 8: *L = make_launch<8, 8, 8, 4, MASS, STIFF>(); return true;
     default: return false;
   }
