@@ -27,6 +27,9 @@
 // atomics).
 #include "fused.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 namespace igs {
 
 bool fused_shape(const igs_problem* p, const Dims& D, FusedShape* fs) {
@@ -105,16 +108,39 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Bulk L2 prefetch (cp.async.bulk.prefetch.L2): keeps the coefficient stream
-// flowing from HBM while the CTA is in its shared-memory-only phases.
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA: one 4D box (points of an element row, 8 lines, 1 layer, all planes).
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
 }
 
 template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
 struct Cfg {
   static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
   static constexpr int NT = 256, NW = NT / 32;
+  static_assert(EX == NW, "warp w owns x-element w of the tile");
   static constexpr int FX = EX + P - 1, FY = EY + P - 1;
   static_assert(EX + 7 <= 16, "x footprint must fit two 8-column MMA tiles");
   static constexpr int RP = 20;               // row pitch (16 used columns, bank-spread)
@@ -122,9 +148,13 @@ struct Cfg {
   static constexpr int TX = EX * Q, TY = EY * Q;
   static_assert(TY % 8 == 0, "lines come in MMA groups of 8");
   static constexpr int TYP = TY + 8;          // lines incl. padding read by Y^T
-  static constexpr int NLG = TY / 8;          // line groups of the X phase
+  static constexpr int NLG = TY / 8;          // line groups = X tasks per warp per layer
   static constexpr int NA = STIFF ? 2 : 1;    // z variants: value, z-derivative
   static constexpr int NV = STIFF ? 3 : 1;    // (y, z) variants: 00, 10, 01
+  static constexpr int NPL = (MASS ? 1 : 0) + (STIFF ? 6 : 0);  // coefficient planes
+  static constexpr int QE = (Q + 1) & ~1;     // TMA box width (16-byte multiple)
+  static constexpr int STG = 3;               // TMA stages per warp
+  static constexpr int FST = NPL * 8 * QE;    // doubles per stage
   static constexpr int LXR = FYP * RP;        // one [n1][n0] plane
   static constexpr int XR = P * LXR;          // x ring (P DoF layers)
   static constexpr int AQ = NA * LXR;         // A for the current q2
@@ -132,30 +162,34 @@ struct Cfg {
   static constexpr int RPT = NV * 8 * EX * TY;  // X^T partials [v][j][ex][line]
   static constexpr int SQ = NA * LXR;         // S for the current q2
   static constexpr int YR = P * LXR;          // y ring
-  static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 128;  // [e][v][q8][j8]
+  static constexpr int TBY = EY * 128, TBZ = 128;  // [e][v][q8][j8]
   static constexpr int WW = TX + TY + 8;
-  static constexpr int TOTAL = XR + AQ + CQ + RPT + SQ + YR + TBX + TBY + TBZ + WW;
-  static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double);
+  static constexpr int FS = NW * STG * FST;   // coefficient staging
+  static constexpr int TOTAL = FS + XR + AQ + CQ + RPT + SQ + YR + TBY + TBZ + WW;
+  static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t);
 };
 
 template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
-__global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
+__global__ void __launch_bounds__(256, 1)
+    apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap) {
   using C = Cfg<P, Q, EX, EY, MASS, STIFF>;
   constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY, TYP = C::TYP;
-  constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR;
-  extern __shared__ double sm[];
-  double* Xr = sm;              // [P][FYP][RP]
+  constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR, STG = C::STG, FST = C::FST, QE = C::QE;
+  constexpr int NLG = C::NLG;
+  extern __shared__ __align__(128) double sm[];
+  double* Fs = sm;              // [NW][STG][NPL][8][QE]  (TMA destination, 128-B aligned)
+  double* Xr = Fs + C::FS;      // [P][FYP][RP]
   double* Aq = Xr + C::XR;      // [NA][FYP][RP]
   double* Cq = Aq + C::AQ;      // [NV][TYP][RP]   (R aliases it)
   double* Rp = Cq + C::CQ;      // [NV][8][EX][TY]
   double* Sq = Rp + C::RPT;     // [NA][FYP][RP]
   double* Yr = Sq + C::SQ;      // [P][FYP][RP]
-  double* Tx = Yr + C::YR;      // [EX][2][8][8]
-  double* Ty = Tx + C::TBX;     // [EY][2][8][8]
+  double* Ty = Yr + C::YR;      // [EY][2][8][8]
   double* Tz = Ty + C::TBY;     // [2][8][8]
   double* Wx = Tz + C::TBZ;     // [TX]
   double* Wy = Wx + TX;         // [TY]
   double* Wz = Wy + TY;         // [8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Wz + 8);  // [NW][STG]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, m = lane & 3;  // MMA fragment coordinates
@@ -168,15 +202,29 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
   const int z1 = min(a.K2, z0 + a.ez);
   double* box = a.scratch + (int64_t)item * a.box;
 
-  // ---- prologue ---------------------------------------------------------------
-  for (int i = tid; i < C::TOTAL; i += NT) sm[i] = 0.0;  // all MMA padding is zero
+  // ---- TMA pipeline: warp w streams the coefficients of x-element w, one
+  // (point layer, 8-line group) box per task, STG tasks ahead.
+  const int ex = warp;             // this warp's element in the tile
+  const int gex = ex0 + ex;
+  const int ntask = (z1 - z0) * Q * NLG;
+  uint64_t* mybar = bars + warp * STG;
+  double* mystage = Fs + warp * STG * FST;
+  auto issue = [&](int idx) {  // lane 0 only
+    const int layer = idx / NLG, lg = idx % NLG;
+    const int zq = z0 * Q + layer;
+    uint64_t* bar = mybar + idx % STG;
+    mbar_expect_tx(bar, (unsigned)(FST * sizeof(double)));
+    tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, gex * Q, ey0 * Q + lg * 8, zq, 0);
+  };
+  if (tid < NW * STG) mbar_init(bars + tid, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
-  for (int i = tid; i < EX * 2 * Q * P; i += NT) {
-    int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
-    int ge = ex0 + e;
-    if (ge < a.K0)
-      Tx[((e * 2 + v) * 8 + q) * 8 + j] = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ge * Q + q];
-  }
+  if (lane == 0)
+    for (int i = 0; i < STG && i < ntask; ++i) issue(i);
+
+  // ---- prologue ---------------------------------------------------------------
+  for (int i = tid; i < C::TOTAL - C::FS; i += NT) Xr[i] = 0.0;  // all MMA padding is zero
+  __syncthreads();
   for (int i = tid; i < EY * 2 * Q * P; i += NT) {
     int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
     int ge = ey0 + e;
@@ -191,6 +239,23 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
     int64_t gg = (int64_t)ey0 * Q + i;
     if (gg < a.X1) Wy[i] = a.wts[1][gg];
   }
+  // This warp's x-element table fragments, kept in registers for the whole
+  // kernel: forward B^T[j][q(n)] and transpose B[q][j] for both levels.
+  double fb0[2], fb1[2], tb0[2], tb1[2];
+  {
+    const int qn = (g >> 1) + 4 * (g & 1);  // D column n -> point q(n)
+    auto tab = [&](int v, int q, int j) -> double {
+      if (gex >= a.K0 || q >= Q || j >= P) return 0.0;
+      return a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)gex * Q + q];
+    };
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      fb0[s] = tab(0, qn, m + 4 * s);
+      fb1[s] = tab(1, qn, m + 4 * s);
+      tb0[s] = tab(0, m + 4 * s, g);
+      tb1[s] = tab(1, m + 4 * s, g);
+    }
+  }
   auto load_layer = [&](int n2) {
     double* dst = Xr + (n2 % P) * LXR;
     for (int i = tid; i < FY * FX; i += NT) {
@@ -203,31 +268,10 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
   };
   for (int l = 0; l < P; ++l) load_layer(z0 + l);
 
-  const double* Fc = MASS ? a.planes + (int64_t)a.pl_c * a.pstride : nullptr;
-  const double* F00 = STIFF ? a.planes + (int64_t)a.pl_a[0][0] * a.pstride : nullptr;
-  const double* F11 = STIFF ? a.planes + (int64_t)a.pl_a[1][1] * a.pstride : nullptr;
-  const double* F22 = STIFF ? a.planes + (int64_t)a.pl_a[2][2] * a.pstride : nullptr;
-  const double* F01 = STIFF ? a.planes + (int64_t)a.pl_a[0][1] * a.pstride : nullptr;
-  const double* F02 = STIFF ? a.planes + (int64_t)a.pl_a[0][2] * a.pstride : nullptr;
-  const double* F12 = STIFF ? a.planes + (int64_t)a.pl_a[1][2] * a.pstride : nullptr;
-  const double* Fpl[7] = {Fc, F00, F11, F22, F01, F02, F12};
-
-  // L2 prefetch of the coefficient rows of slab-local point layer zq.
-  const int nvalid_el_x = min(EX, a.K0 - ex0), nvalid_el_y = min(EY, a.K1 - ey0);
-  auto prefetch_layer = [&](int64_t zq) {
-    constexpr int NPL = 7;
-    const int rows = nvalid_el_y * Q;
-    const unsigned bytes = (unsigned)(nvalid_el_x * Q * sizeof(double));
-    for (int i = tid; i < NPL * rows; i += NT) {
-      int pl = i / rows, line = i % rows;
-      if (!Fpl[pl]) continue;
-      const double* p = Fpl[pl] + (zq * a.X1 + (int64_t)ey0 * Q + line) * a.X0 + (int64_t)ex0 * Q;
-      if (((uintptr_t)p & 15) == 0 && (bytes & 15) == 0) prefetch_l2(p, bytes);
-    }
-  };
-  const int64_t zq_end = (int64_t)z1 * Q;
-  prefetch_layer((int64_t)z0 * Q);
-  if (Q > 1 || z0 + 1 < z1) prefetch_layer((int64_t)z0 * Q + 1);
+  // plane slots inside a TMA stage
+  const int pc = a.pl_c;
+  const int p00 = a.pl_a[0][0], p11 = a.pl_a[1][1], p22 = a.pl_a[2][2];
+  const int p01 = a.pl_a[0][1], p02 = a.pl_a[0][2], p12 = a.pl_a[1][2];
 
   // Z^T of point layer q2 of the current element into the y ring (same item
   // mapping as the Z phase, so each (n1, n0) is owned by one thread).
@@ -244,6 +288,7 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
     }
   };
 
+  int widx = 0;  // this warp's running task index (TMA ring position)
   for (int e2 = z0; e2 < z1; ++e2) {
     const int gz = e2 + a.z_el_off;
     for (int i = tid; i < 2 * Q * P; i += NT) {
@@ -254,7 +299,6 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
     __syncthreads();
 
     for (int q2 = 0; q2 < Q; ++q2) {
-      const int64_t zq = (int64_t)e2 * Q + q2;  // slab-local point layer
       // ---- Z^T(q2-1) + Z(q2) + clear S ---------------------------------------
       for (int i = tid; i < FY * FX; i += NT) {
         if (q2 > 0) zt_item(e2, q2 - 1, i);
@@ -273,7 +317,6 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
           Sq[LXR + o] = 0.0;
         }
       }
-      if (zq + 2 < zq_end) prefetch_layer(zq + 2);
       __syncthreads();
 
       // ---- Y (DMMA): C_vw[q1][n0] = Σ_j By_w[q1][j] · A_v[ey+j][n0] ----------
@@ -307,33 +350,30 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
       }
       __syncthreads();
 
-      // ---- X (DMMA) + pointwise + X^T (DMMA): task = (element ex, 8 lines) ----
-      for (int t = warp; t < EX * C::NLG; t += NW) {
-        const int ex = t % EX, lg = t / EX;
+      // ---- X (DMMA) + pointwise + X^T (DMMA): warp = element, task = 8 lines --
+      for (int lg = 0; lg < NLG; ++lg, ++widx) {
         const int line = lg * 8 + g;  // A-fragment / D row
-        const int gex = ex0 + ex;
-        // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q];
-        // D column n holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two
-        // D values are points q = m and q = m + 4 -- exactly the A-fragment
-        // columns of the transposed product below (no shuffles needed).
-        const int qn = (g >> 1) + 4 * (g & 1);
+        // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q];  D column n
+        // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
+        // are points q = m and m + 4: the A-fragment columns of the transposed
+        // product below (no shuffles).
         double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int j = m + 4 * s;
-          const double b0 = Tx[((ex * 2 + 0) * 8 + qn) * 8 + j];
           const double c0 = Cq[line * RP + ex + j];
-          if (MASS) dmma(u[0], u[1], c0, b0);
+          if (MASS) dmma(u[0], u[1], c0, fb0[s]);
           if (STIFF) {
-            const double b1 = Tx[((ex * 2 + 1) * 8 + qn) * 8 + j];
             const double c1 = Cq[TYP * RP + line * RP + ex + j];
             const double c2 = Cq[2 * TYP * RP + line * RP + ex + j];
-            dmma(ux[0], ux[1], c0, b1);
-            dmma(uy[0], uy[1], c1, b0);
-            dmma(uz[0], uz[1], c2, b0);
+            dmma(ux[0], ux[1], c0, fb1[s]);
+            dmma(uy[0], uy[1], c1, fb0[s]);
+            dmma(uz[0], uz[1], c2, fb0[s]);
           }
         }
-        // pointwise: g = w · F(x) · (u, ∇u) at points (line, m) and (line, m+4)
+        // coefficients of this task (TMA stage)
+        mbar_wait(mybar + widx % STG, (unsigned)((widx / STG) & 1));
+        const double* F = mystage + (widx % STG) * FST;
         const bool row_ok = gex < a.K0 && (ey0 + line / Q) < a.K1;
         double g0[2], gx[2], gy[2], gz[2];
 #pragma unroll
@@ -341,30 +381,32 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
           const int q = m + 4 * c;
           g0[c] = gx[c] = gy[c] = gz[c] = 0.0;
           if (q < Q && row_ok) {
-            const int64_t fo = (zq * a.X1 + (int64_t)ey0 * Q + line) * a.X0 + (int64_t)gex * Q + q;
+            const double* f = F + g * QE + q;  // [plane][line][q]
             const double w = Wz[q2] * Wy[line] * Wx[ex * Q + q];
-            if (MASS) g0[c] = w * (__ldg(Fc + fo) * u[c]);
+            if (MASS) g0[c] = w * (f[pc * 8 * QE] * u[c]);
             if (STIFF) {
-              const double f00 = __ldg(F00 + fo), f11 = __ldg(F11 + fo), f22 = __ldg(F22 + fo);
-              const double f01 = __ldg(F01 + fo), f02 = __ldg(F02 + fo), f12 = __ldg(F12 + fo);
+              const double f00 = f[p00 * 8 * QE], f11 = f[p11 * 8 * QE], f22 = f[p22 * 8 * QE];
+              const double f01 = f[p01 * 8 * QE], f02 = f[p02 * 8 * QE], f12 = f[p12 * 8 * QE];
               gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
               gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
               gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
             }
           }
         }
+        __syncwarp();
+        if (lane == 0 && widx + STG < ntask) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(widx + STG);
+        }
         // transpose: R^T[line][j] = Σ_q g^T[line][q] · B[q][j]
         double r00[2] = {0.0, 0.0}, r10[2] = {0.0, 0.0}, r01[2] = {0.0, 0.0};
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          const int q = m + 4 * s;
-          const double b0 = Tx[((ex * 2 + 0) * 8 + q) * 8 + g];
-          if (MASS) dmma(r00[0], r00[1], g0[s], b0);
+          if (MASS) dmma(r00[0], r00[1], g0[s], tb0[s]);
           if (STIFF) {
-            const double b1 = Tx[((ex * 2 + 1) * 8 + q) * 8 + g];
-            dmma(r00[0], r00[1], gx[s], b1);
-            dmma(r10[0], r10[1], gy[s], b0);
-            dmma(r01[0], r01[1], gz[s], b0);
+            dmma(r00[0], r00[1], gx[s], tb1[s]);
+            dmma(r10[0], r10[1], gy[s], tb0[s]);
+            dmma(r01[0], r01[1], gz[s], tb0[s]);
           }
         }
         // partials Rp[v][j][ex][line] with j = 2m + c
@@ -436,7 +478,6 @@ __global__ void __launch_bounds__(256, 2) apply3d_kernel(const ApplyArgs a) {
       box[(int64_t)(e2 - z0) * FY * FX + i] = *yr;
       *yr = 0.0;
     }
-    __syncthreads();
     load_layer(e2 + P);
     __syncthreads();
   }
@@ -498,15 +539,15 @@ __global__ void apply_reduce_kernel(const ReduceArgs r) {
 // ---- instantiation table ----------------------------------------------------
 
 struct Launch {
-  int EX, EY, NT;
+  int EX, EY, NT, NPL, QE;
   size_t smem;
-  void (*kernel)(ApplyArgs);
+  void (*kernel)(ApplyArgs, CUtensorMap);
 };
 
 template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
 Launch make_launch() {
   using C = Cfg<P, Q, EX, EY, MASS, STIFF>;
-  return Launch{EX, EY, C::NT, C::SMEM, &apply3d_kernel<P, Q, EX, EY, MASS, STIFF>};
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, MASS, STIFF>};
 }
 
 // Tile shapes per order (256 threads; EY·Q lines must be a multiple of 8).
@@ -527,10 +568,12 @@ bool pick(int P, int Q, Launch* L) {
 
 bool pick_launch(const FusedShape& s, Launch* L) {
   if (s.d != 3) return false;
-  if (s.mass && s.stiff) return pick<true, true>(s.p, s.k, L);
-  if (s.stiff) return pick<false, true>(s.p, s.k, L);
-  if (s.mass) return pick<true, false>(s.p, s.k, L);
-  return false;
+  bool ok = false;
+  if (s.mass && s.stiff) ok = pick<true, true>(s.p, s.k, L);
+  else if (s.stiff) ok = pick<false, true>(s.p, s.k, L);
+  else if (s.mass) ok = pick<true, false>(s.p, s.k, L);
+  // 227 KB of dynamic shared memory per CTA on sm_100a
+  return ok && L->smem <= 232448;
 }
 
 struct Tiling {
@@ -558,13 +601,45 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
   return t;
 }
 
+// The coefficient planes as one 4D tensor (x, y, z points, plane) for TMA.
+// cuTensorMapEncodeTiled comes from the driver through the runtime's entry
+// point query, so the library does not link libcuda directly.
+igs_status coeff_tensor_map(CUtensorMap* map, const double* planes, int64_t pstride, const Dims& D,
+                            const Launch& L) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(IGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)D.x[0], (cuuint64_t)D.x[1], (cuuint64_t)D.x[2], (cuuint64_t)L.NPL};
+  cuuint64_t strides[3] = {(cuuint64_t)D.x[0] * 8, (cuuint64_t)(D.x[0] * D.x[1]) * 8, (cuuint64_t)pstride * 8};
+  cuuint32_t boxd[4] = {(cuuint32_t)L.QE, 8u, 1u, (cuuint32_t)L.NPL};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(planes), dims, strides,
+                      boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(IGS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return IGS_OK;
+}
+
+// TMA needs 16-byte aligned rows/planes and exactly the kernel's plane set.
+bool tma_ok(const igs_problem* p, const Dims& D, const Launch& L) {
+  if ((D.x[0] * 8) % 16 != 0 || (p->plane_stride * 8) % 16 != 0) return false;
+  if (p->n_planes != L.NPL) return false;
+  return true;
+}
+
 }  // namespace
 
 bool fused_apply_supported(const igs_problem* p, const Dims& D) {
   FusedShape s;
   if (!fused_shape(p, D, &s)) return false;
   Launch L;
-  return pick_launch(s, &L);
+  return pick_launch(s, &L) && tma_ok(p, D, L);
 }
 
 size_t fused_apply_workspace(const igs_problem* p, const Dims& D) {
@@ -579,7 +654,9 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
                        double* y, void* ws, size_t ws_bytes, int flags, cudaStream_t st) {
   FusedShape s;
   Launch L;
-  if (!fused_shape(p, D, &s) || !pick_launch(s, &L)) return fail(IGS_ECAPACITY, "no fused apply");
+  if (!fused_shape(p, D, &s) || !pick_launch(s, &L) || !tma_ok(p, D, L))
+    return fail(IGS_ECAPACITY, "no fused apply");
+  if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
   Tiling t = tiling(s, L);
   size_t need = (size_t)t.ntx * t.nty * t.nch * t.box * sizeof(double);
   if (ws_bytes < need || !ws) return fail(IGS_EWORKSPACE, "workspace too small for the fused apply");
@@ -602,10 +679,12 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
   a.ntx = t.ntx; a.nty = t.nty; a.nch = t.nch; a.ez = t.ez;
   a.scratch = reinterpret_cast<double*>(ws);
   a.box = t.box;
+  CUtensorMap fmap;
+  IGS_TRY(coeff_tensor_map(&fmap, planes, p->plane_stride, D, L));
   IGS_TRY(cuda_check(cudaFuncSetAttribute(L.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)L.smem), "smem attribute"));
   unsigned grid = (unsigned)(t.ntx * t.nty * t.nch);
-  L.kernel<<<grid, L.NT, L.smem, st>>>(a);
+  L.kernel<<<grid, L.NT, L.smem, st>>>(a, fmap);
   IGS_LAUNCH_CHECK("apply3d_kernel");
   if (flags & IGS_FLAG_KERNEL_ONLY) return IGS_OK;
   ReduceArgs r{};
