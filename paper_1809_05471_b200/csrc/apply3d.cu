@@ -126,7 +126,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// TMA: one 4D box (points of an element row, 8 lines, 1 layer, all planes).
+// TMA: one 4D box (points of one element, 8 lines, 1 point layer, all planes).
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
   asm volatile(
@@ -136,55 +136,59 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
+// Tile geometry and shared-memory plan.  Q2B point layers of z are processed
+// per batch; warp w owns (point layer w / NLG of the batch, line group
+// w % NLG) in the X phase and sweeps all EX elements of its 8 lines.
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF>
 struct Cfg {
   static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
-  static constexpr int NT = 256, NW = NT / 32;
-  static_assert(EX == NW, "warp w owns x-element w of the tile");
+  static_assert(Q % Q2B == 0, "batches tile the element's point layers");
   static constexpr int FX = EX + P - 1, FY = EY + P - 1;
   static_assert(EX + 7 <= 16, "x footprint must fit two 8-column MMA tiles");
-  static constexpr int RP = 20;               // row pitch (16 used columns, bank-spread)
-  static constexpr int FYP = EY + 8;          // rows incl. MMA padding
+  static constexpr int RP = 20;                // row pitch (16 used columns, bank-spread)
+  static constexpr int FYP = EY + 8;           // rows incl. MMA padding
   static constexpr int TX = EX * Q, TY = EY * Q;
   static_assert(TY % 8 == 0, "lines come in MMA groups of 8");
-  static constexpr int TYP = TY + 8;          // lines incl. padding read by Y^T
-  static constexpr int NLG = TY / 8;          // line groups = X tasks per warp per layer
-  static constexpr int NA = STIFF ? 2 : 1;    // z variants: value, z-derivative
-  static constexpr int NV = STIFF ? 3 : 1;    // (y, z) variants: 00, 10, 01
+  static constexpr int TYP = TY + 8;           // lines incl. padding read by Y^T
+  static constexpr int NLG = TY / 8;           // line groups
+  static constexpr int NW = Q2B * NLG, NT = 32 * NW;
+  static constexpr int NB = Q / Q2B;           // batches per element layer
+  static constexpr int NA = STIFF ? 2 : 1;     // z variants: value, z-derivative
+  static constexpr int NV = STIFF ? 3 : 1;     // (y, z) variants: 00, 10, 01
   static constexpr int NPL = (MASS ? 1 : 0) + (STIFF ? 6 : 0);  // coefficient planes
-  static constexpr int QE = (Q + 1) & ~1;     // TMA box width (16-byte multiple)
-  static constexpr int STG = 3;               // TMA stages per warp
-  static constexpr int FST = NPL * 8 * QE;    // doubles per stage
-  static constexpr int LXR = FYP * RP;        // one [n1][n0] plane
-  static constexpr int XR = P * LXR;          // x ring (P DoF layers)
-  static constexpr int AQ = NA * LXR;         // A for the current q2
-  static constexpr int CQ = NV * TYP * RP;    // C for the current q2, then R
-  static constexpr int RPT = NV * 8 * EX * TY;  // X^T partials [v][j][ex][line]
-  static constexpr int SQ = NA * LXR;         // S for the current q2
-  static constexpr int YR = P * LXR;          // y ring
-  static constexpr int TBY = EY * 128, TBZ = 128;  // [e][v][q8][j8]
+  static constexpr int QE = (Q + 1) & ~1;      // TMA box width (16-byte multiple)
+  static constexpr int STG = 3;                // TMA stages per warp
+  static constexpr int FST = NPL * 8 * QE;     // doubles per stage
+  static constexpr int LXR = FYP * RP;         // one [n1][n0] plane
+  static constexpr int XR = P * LXR;           // x ring (P DoF layers)
+  static constexpr int AQ = Q2B * NA * LXR;    // A per point layer of the batch
+  static constexpr int CQL = TYP * RP;         // one C/R variant plane
+  static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
+  static constexpr int SQ = Q2B * NA * LXR;    // S per point layer of the batch
+  static constexpr int YR = P * LXR;           // y ring
+  static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 128;  // [e][v][q8][j8]
   static constexpr int WW = TX + TY + 8;
-  static constexpr int FS = NW * STG * FST;   // coefficient staging
-  static constexpr int TOTAL = FS + XR + AQ + CQ + RPT + SQ + YR + TBY + TBZ + WW;
+  static constexpr int FS = NW * STG * FST;    // coefficient staging
+  static constexpr int TOTAL = FS + XR + AQ + CQ + SQ + YR + TBX + TBY + TBZ + WW;
   static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t);
 };
 
-template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
-__global__ void __launch_bounds__(256, 1)
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF>
+__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
     apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap) {
-  using C = Cfg<P, Q, EX, EY, MASS, STIFF>;
-  constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY, TYP = C::TYP;
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>;
+  constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY;
   constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR, STG = C::STG, FST = C::FST, QE = C::QE;
-  constexpr int NLG = C::NLG;
+  constexpr int NLG = C::NLG, NB = C::NB, CQL = C::CQL, NA = C::NA, NV = C::NV;
   extern __shared__ __align__(128) double sm[];
-  double* Fs = sm;              // [NW][STG][NPL][8][QE]  (TMA destination, 128-B aligned)
+  double* Fs = sm;              // [NW][STG][NPL][8][QE]  (TMA destination)
   double* Xr = Fs + C::FS;      // [P][FYP][RP]
-  double* Aq = Xr + C::XR;      // [NA][FYP][RP]
-  double* Cq = Aq + C::AQ;      // [NV][TYP][RP]   (R aliases it)
-  double* Rp = Cq + C::CQ;      // [NV][8][EX][TY]
-  double* Sq = Rp + C::RPT;     // [NA][FYP][RP]
+  double* Aq = Xr + C::XR;      // [Q2B][NA][FYP][RP]
+  double* Cq = Aq + C::AQ;      // [Q2B][NV][TYP][RP]   (R overwrites C in place)
+  double* Sq = Cq + C::CQ;      // [Q2B][NA][FYP][RP]
   double* Yr = Sq + C::SQ;      // [P][FYP][RP]
-  double* Ty = Yr + C::YR;      // [EY][2][8][8]
+  double* Tx = Yr + C::YR;      // [EX][2][8][8]
+  double* Ty = Tx + C::TBX;     // [EY][2][8][8]
   double* Tz = Ty + C::TBY;     // [2][8][8]
   double* Wx = Tz + C::TBZ;     // [TX]
   double* Wy = Wx + TX;         // [TY]
@@ -202,19 +206,19 @@ __global__ void __launch_bounds__(256, 1)
   const int z1 = min(a.K2, z0 + a.ez);
   double* box = a.scratch + (int64_t)item * a.box;
 
-  // ---- TMA pipeline: warp w streams the coefficients of x-element w, one
-  // (point layer, 8-line group) box per task, STG tasks ahead.
-  const int ex = warp;             // this warp's element in the tile
-  const int gex = ex0 + ex;
-  const int ntask = (z1 - z0) * Q * NLG;
+  // ---- coefficient stream: warp w's X task in every batch covers point
+  // layer (batch·Q2B + w/NLG) and line group w%NLG, element by element; each
+  // (batch, element) is one TMA box, STG boxes in flight per warp.
+  const int wq = warp / NLG, wlg = warp % NLG;
+  const int ntask = (z1 - z0) * NB * EX;
   uint64_t* mybar = bars + warp * STG;
   double* mystage = Fs + warp * STG * FST;
-  auto issue = [&](int idx) {  // lane 0 only
-    const int layer = idx / NLG, lg = idx % NLG;
-    const int zq = z0 * Q + layer;
+  auto issue = [&](int idx) {  // one lane
+    const int batch = idx / EX, ex = idx % EX;
+    const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
     uint64_t* bar = mybar + idx % STG;
     mbar_expect_tx(bar, (unsigned)(FST * sizeof(double)));
-    tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, gex * Q, ey0 * Q + lg * 8, zq, 0);
+    tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + ex) * Q, ey0 * Q + wlg * 8, zq, 0);
   };
   if (tid < NW * STG) mbar_init(bars + tid, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -225,6 +229,12 @@ __global__ void __launch_bounds__(256, 1)
   // ---- prologue ---------------------------------------------------------------
   for (int i = tid; i < C::TOTAL - C::FS; i += NT) Xr[i] = 0.0;  // all MMA padding is zero
   __syncthreads();
+  for (int i = tid; i < EX * 2 * Q * P; i += NT) {
+    int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
+    int ge = ex0 + e;
+    if (ge < a.K0)
+      Tx[((e * 2 + v) * 8 + q) * 8 + j] = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ge * Q + q];
+  }
   for (int i = tid; i < EY * 2 * Q * P; i += NT) {
     int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
     int ge = ey0 + e;
@@ -238,23 +248,6 @@ __global__ void __launch_bounds__(256, 1)
   for (int i = tid; i < TY; i += NT) {
     int64_t gg = (int64_t)ey0 * Q + i;
     if (gg < a.X1) Wy[i] = a.wts[1][gg];
-  }
-  // This warp's x-element table fragments, kept in registers for the whole
-  // kernel: forward B^T[j][q(n)] and transpose B[q][j] for both levels.
-  double fb0[2], fb1[2], tb0[2], tb1[2];
-  {
-    const int qn = (g >> 1) + 4 * (g & 1);  // D column n -> point q(n)
-    auto tab = [&](int v, int q, int j) -> double {
-      if (gex >= a.K0 || q >= Q || j >= P) return 0.0;
-      return a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)gex * Q + q];
-    };
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      fb0[s] = tab(0, qn, m + 4 * s);
-      fb1[s] = tab(1, qn, m + 4 * s);
-      tb0[s] = tab(0, m + 4 * s, g);
-      tb1[s] = tab(1, m + 4 * s, g);
-    }
   }
   auto load_layer = [&](int n2) {
     double* dst = Xr + (n2 % P) * LXR;
@@ -273,22 +266,30 @@ __global__ void __launch_bounds__(256, 1)
   const int p00 = a.pl_a[0][0], p11 = a.pl_a[1][1], p22 = a.pl_a[2][2];
   const int p01 = a.pl_a[0][1], p02 = a.pl_a[0][2], p12 = a.pl_a[1][2];
 
-  // Z^T of point layer q2 of the current element into the y ring (same item
-  // mapping as the Z phase, so each (n1, n0) is owned by one thread).
-  auto zt_item = [&](int e2, int q2, int i) {
-    int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
-    double s0 = Sq[o];
-    double s1 = STIFF ? Sq[LXR + o] : 0.0;
+  // Z^T of the Q2B point layers of batch `b` into the y ring (item mapping
+  // (n1, n0) identical in every phase that touches the ring).
+  auto zt_item = [&](int e2, int b, int i) {
+    const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
+    double* yrow[P];
 #pragma unroll
-    for (int j = 0; j < P; ++j) {
-      double* yr = Yr + ((e2 + j) % P) * LXR + o;
-      double v = fma(Tz[(0 * 8 + q2) * 8 + j], s0, *yr);
-      if (STIFF) v = fma(Tz[(1 * 8 + q2) * 8 + j], s1, v);
-      *yr = v;
+    for (int j = 0; j < P; ++j) yrow[j] = Yr + ((e2 + j) % P) * LXR + o;
+#pragma unroll
+    for (int qb = 0; qb < Q2B; ++qb) {
+      const int q2 = b * Q2B + qb;
+      const double s0 = Sq[(qb * NA + 0) * LXR + o];
+      const double s1 = STIFF ? Sq[(qb * NA + 1) * LXR + o] : 0.0;
+      Sq[(qb * NA + 0) * LXR + o] = 0.0;
+      if (STIFF) Sq[(qb * NA + 1) * LXR + o] = 0.0;
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        double v = fma(Tz[(0 * 8 + q2) * 8 + j], s0, *yrow[j]);
+        if (STIFF) v = fma(Tz[(1 * 8 + q2) * 8 + j], s1, v);
+        *yrow[j] = v;
+      }
     }
   };
 
-  int widx = 0;  // this warp's running task index (TMA ring position)
+  int widx = 0;  // this warp's running TMA task index
   for (int e2 = z0; e2 < z1; ++e2) {
     const int gz = e2 + a.z_el_off;
     for (int i = tid; i < 2 * Q * P; i += NT) {
@@ -298,171 +299,194 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = tid; i < Q; i += NT) Wz[i] = a.wts[2][(int64_t)gz * Q + i];
     __syncthreads();
 
-    for (int q2 = 0; q2 < Q; ++q2) {
-      // ---- Z^T(q2-1) + Z(q2) + clear S ---------------------------------------
-      for (int i = tid; i < FY * FX; i += NT) {
-        if (q2 > 0) zt_item(e2, q2 - 1, i);
-        int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
+    for (int b = 0; b < NB; ++b) {
+      // ---- Z^T(previous batch) + Z(this batch) + clear S ---------------------
+      if (b > 0)
+        for (int i = tid; i < FY * FX; i += NT) zt_item(e2, b - 1, i);
+      for (int i = tid; i < Q2B * FY * FX; i += NT) {
+        const int qb = i / (FY * FX), r = i % (FY * FX);
+        const int n0 = r % FX, n1 = r / FX, o = n1 * RP + n0;
+        const int q2 = b * Q2B + qb;
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
         for (int j = 0; j < P; ++j) {
-          double xv = Xr[((e2 + j) % P) * LXR + o];
+          const double xv = Xr[((e2 + j) % P) * LXR + o];
           a0 = fma(Tz[(0 * 8 + q2) * 8 + j], xv, a0);
           if (STIFF) a1 = fma(Tz[(1 * 8 + q2) * 8 + j], xv, a1);
         }
-        Aq[o] = a0;
-        Sq[o] = 0.0;
-        if (STIFF) {
-          Aq[LXR + o] = a1;
-          Sq[LXR + o] = 0.0;
-        }
+        Aq[(qb * NA + 0) * LXR + o] = a0;
+        if (STIFF) Aq[(qb * NA + 1) * LXR + o] = a1;
       }
       __syncthreads();
 
       // ---- Y (DMMA): C_vw[q1][n0] = Σ_j By_w[q1][j] · A_v[ey+j][n0] ----------
-      for (int t = warp; t < EY * 2; t += NW) {
-        const int ey = t >> 1, nt = t & 1;
+      for (int t = warp; t < Q2B * EY * 2; t += NW) {
+        const int qb = t / (EY * 2), ey = (t / 2) % EY, nt = t & 1;
+        const double* A0 = Aq + (qb * NA + 0) * LXR;
         double c00[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0};
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int j = m + 4 * s;
           const double t0 = Ty[((ey * 2 + 0) * 8 + g) * 8 + j];
-          const double b0 = Aq[(ey + j) * RP + nt * 8 + g];
+          const double b0 = A0[(ey + j) * RP + nt * 8 + g];
           dmma(c00[0], c00[1], t0, b0);
           if (STIFF) {
             const double t1 = Ty[((ey * 2 + 1) * 8 + g) * 8 + j];
-            const double b1 = Aq[LXR + (ey + j) * RP + nt * 8 + g];
+            const double b1 = A0[LXR + (ey + j) * RP + nt * 8 + g];
             dmma(c10[0], c10[1], t1, b0);
             dmma(c01[0], c01[1], t0, b1);
           }
         }
         if (g < Q) {
+          double* Cb = Cq + qb * NV * CQL;
           const int o = (ey * Q + g) * RP + nt * 8 + 2 * m;
-          Cq[o] = c00[0];
-          Cq[o + 1] = c00[1];
+          Cb[o] = c00[0];
+          Cb[o + 1] = c00[1];
           if (STIFF) {
-            Cq[TYP * RP + o] = c10[0];
-            Cq[TYP * RP + o + 1] = c10[1];
-            Cq[2 * TYP * RP + o] = c01[0];
-            Cq[2 * TYP * RP + o + 1] = c01[1];
+            Cb[CQL + o] = c10[0];
+            Cb[CQL + o + 1] = c10[1];
+            Cb[2 * CQL + o] = c01[0];
+            Cb[2 * CQL + o + 1] = c01[1];
           }
         }
       }
       __syncthreads();
 
-      // ---- X (DMMA) + pointwise + X^T (DMMA): warp = element, task = 8 lines --
-      for (int lg = 0; lg < NLG; ++lg, ++widx) {
-        const int line = lg * 8 + g;  // A-fragment / D row
-        // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q];  D column n
-        // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
-        // are points q = m and m + 4: the A-fragment columns of the transposed
-        // product below (no shuffles).
-        double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
+      // ---- X (DMMA) + pointwise + X^T (DMMA), warp-private rows ---------------
+      {
+        const int q2 = b * Q2B + wq;
+        const int line = wlg * 8 + g;   // A-fragment / D row
+        double* Cb = Cq + wq * NV * CQL;
+        double* Crow = Cb + line * RP;  // C (then R) row of this lane's line
+        const bool line_ok = (ey0 + line / Q) < a.K1;
+        const double wyz = Wz[q2] * Wy[line];
+        // running X^T window over columns [ex, ex+8): lane m holds ex+2m, ex+2m+1
+        double w00[2] = {0.0, 0.0}, w10[2] = {0.0, 0.0}, w01[2] = {0.0, 0.0};
+        const int qn = (g >> 1) + 4 * (g & 1);  // D column n -> point q(n)
+#pragma unroll 2
+        for (int ex = 0; ex < EX; ++ex, ++widx) {
+          const double* T0 = Tx + (ex * 2 + 0) * 64;
+          const double* T1 = Tx + (ex * 2 + 1) * 64;
+          // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  D column n
+          // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
+          // are points q = m and m + 4: the A-fragment columns of the
+          // transposed product below (no shuffles).
+          double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const int j = m + 4 * s;
-          const double c0 = Cq[line * RP + ex + j];
-          if (MASS) dmma(u[0], u[1], c0, fb0[s]);
-          if (STIFF) {
-            const double c1 = Cq[TYP * RP + line * RP + ex + j];
-            const double c2 = Cq[2 * TYP * RP + line * RP + ex + j];
-            dmma(ux[0], ux[1], c0, fb1[s]);
-            dmma(uy[0], uy[1], c1, fb0[s]);
-            dmma(uz[0], uz[1], c2, fb0[s]);
-          }
-        }
-        // coefficients of this task (TMA stage)
-        mbar_wait(mybar + widx % STG, (unsigned)((widx / STG) & 1));
-        const double* F = mystage + (widx % STG) * FST;
-        const bool row_ok = gex < a.K0 && (ey0 + line / Q) < a.K1;
-        double g0[2], gx[2], gy[2], gz[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int q = m + 4 * c;
-          g0[c] = gx[c] = gy[c] = gz[c] = 0.0;
-          if (q < Q && row_ok) {
-            const double* f = F + g * QE + q;  // [plane][line][q]
-            const double w = Wz[q2] * Wy[line] * Wx[ex * Q + q];
-            if (MASS) g0[c] = w * (f[pc * 8 * QE] * u[c]);
+          for (int s = 0; s < 2; ++s) {
+            const int j = m + 4 * s;
+            const double fb0 = T0[qn * 8 + j];
+            const double c0 = Crow[ex + j];
+            if (MASS) dmma(u[0], u[1], c0, fb0);
             if (STIFF) {
-              const double f00 = f[p00 * 8 * QE], f11 = f[p11 * 8 * QE], f22 = f[p22 * 8 * QE];
-              const double f01 = f[p01 * 8 * QE], f02 = f[p02 * 8 * QE], f12 = f[p12 * 8 * QE];
-              gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
-              gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
-              gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
+              const double fb1 = T1[qn * 8 + j];
+              const double c1 = Crow[CQL + ex + j];
+              const double c2 = Crow[2 * CQL + ex + j];
+              dmma(ux[0], ux[1], c0, fb1);
+              dmma(uy[0], uy[1], c1, fb0);
+              dmma(uz[0], uz[1], c2, fb0);
+            }
+          }
+          // coefficients of (element ex, these 8 lines, point layer q2)
+          mbar_wait(mybar + widx % STG, (unsigned)((widx / STG) & 1));
+          const double* F = mystage + (widx % STG) * FST;
+          const bool ok = (ex0 + ex) < a.K0 && line_ok;
+          double g0[2], gx[2], gy[2], gz[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int q = m + 4 * c;
+            g0[c] = gx[c] = gy[c] = gz[c] = 0.0;
+            if (q < Q && ok) {
+              const double* f = F + g * QE + q;  // [plane][line][q]
+              const double w = wyz * Wx[ex * Q + q];
+              if (MASS) g0[c] = w * (f[pc * 8 * QE] * u[c]);
+              if (STIFF) {
+                const double f00 = f[p00 * 8 * QE], f11 = f[p11 * 8 * QE], f22 = f[p22 * 8 * QE];
+                const double f01 = f[p01 * 8 * QE], f02 = f[p02 * 8 * QE], f12 = f[p12 * 8 * QE];
+                gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
+                gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
+                gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0 && widx + STG < ntask) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(widx + STG);
+          }
+          // transpose into the window: W^T[line][j] += Σ_q g^T[line][q] · B[q][j]
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int q = m + 4 * s;
+            const double tb0 = T0[q * 8 + g];
+            if (MASS) dmma(w00[0], w00[1], g0[s], tb0);
+            if (STIFF) {
+              const double tb1 = T1[q * 8 + g];
+              dmma(w00[0], w00[1], gx[s], tb1);
+              dmma(w10[0], w10[1], gy[s], tb0);
+              dmma(w01[0], w01[1], gz[s], tb0);
+            }
+          }
+          // column ex is complete (no later element touches it): store it over
+          // C's column ex, which no later element reads, then slide the window.
+          __syncwarp();
+          if (m == 0) {
+            Crow[ex] = w00[0];
+            if (STIFF) {
+              Crow[CQL + ex] = w10[0];
+              Crow[2 * CQL + ex] = w01[0];
+            }
+          }
+          {
+            double nx = __shfl_down_sync(0xffffffffu, w00[0], 1, 4);
+            w00[0] = w00[1];
+            w00[1] = (m == 3) ? 0.0 : nx;
+            if (STIFF) {
+              nx = __shfl_down_sync(0xffffffffu, w10[0], 1, 4);
+              w10[0] = w10[1];
+              w10[1] = (m == 3) ? 0.0 : nx;
+              nx = __shfl_down_sync(0xffffffffu, w01[0], 1, 4);
+              w01[0] = w01[1];
+              w01[1] = (m == 3) ? 0.0 : nx;
             }
           }
         }
+        // remaining columns [EX, EX + 8): lane m holds EX + 2m + c
         __syncwarp();
-        if (lane == 0 && widx + STG < ntask) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(widx + STG);
-        }
-        // transpose: R^T[line][j] = Σ_q g^T[line][q] · B[q][j]
-        double r00[2] = {0.0, 0.0}, r10[2] = {0.0, 0.0}, r01[2] = {0.0, 0.0};
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          if (MASS) dmma(r00[0], r00[1], g0[s], tb0[s]);
-          if (STIFF) {
-            dmma(r00[0], r00[1], gx[s], tb1[s]);
-            dmma(r10[0], r10[1], gy[s], tb0[s]);
-            dmma(r01[0], r01[1], gz[s], tb0[s]);
-          }
-        }
-        // partials Rp[v][j][ex][line] with j = 2m + c
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int o = ((2 * m + c) * EX + ex) * TY + line;
-          Rp[o] = r00[c];
-          if (STIFF) {
-            Rp[8 * EX * TY + o] = r10[c];
-            Rp[2 * 8 * EX * TY + o] = r01[c];
+          const int col = EX + 2 * m + c;
+          if (col < FX) {
+            Crow[col] = w00[c];
+            if (STIFF) {
+              Crow[CQL + col] = w10[c];
+              Crow[2 * CQL + col] = w01[c];
+            }
           }
-        }
-      }
-      __syncthreads();
-
-      // ---- X^T overlap-add: R_v[line][n0] = Σ_s partial(ex = n0 - s, j = s) -----
-      for (int i = tid; i < TY * FX; i += NT) {
-        const int line = i % TY, n0 = i / TY;
-        const int s_lo = n0 - (EX - 1) > 0 ? n0 - (EX - 1) : 0;
-        const int s_hi = n0 < 7 ? n0 : 7;
-        double r00 = 0.0, r10 = 0.0, r01 = 0.0;
-        for (int s = s_lo; s <= s_hi; ++s) {
-          const int o = (s * EX + (n0 - s)) * TY + line;
-          r00 += Rp[o];
-          if (STIFF) {
-            r10 += Rp[8 * EX * TY + o];
-            r01 += Rp[2 * 8 * EX * TY + o];
-          }
-        }
-        Cq[line * RP + n0] = r00;
-        if (STIFF) {
-          Cq[TYP * RP + line * RP + n0] = r10;
-          Cq[2 * TYP * RP + line * RP + n0] = r01;
         }
       }
       __syncthreads();
 
       // ---- Y^T (DMMA): S_v[ey+j][n0] += Σ_q By[q][j] · R[ey*Q+q][n0] ----------
-      for (int t = warp; t < C::NA * 2; t += NW) {
-        const int grp = t >> 1, nt = t & 1;
+      for (int t = warp; t < Q2B * NA * 2; t += NW) {
+        const int qb = t / (NA * 2), grp = (t / 2) % NA, nt = t & 1;
+        const double* Rb = Cq + qb * NV * CQL;
+        double* Sb = Sq + (qb * NA + grp) * LXR;
         for (int ey = 0; ey < EY; ++ey) {
           double d[2] = {0.0, 0.0};
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             const int q = m + 4 * s;
-            const int line = ey * Q + q;  // < TYP (padding rows are zero)
+            const int o = (ey * Q + q) * RP + nt * 8 + g;  // rows < TYP (padding zero)
             const double t0 = Ty[((ey * 2 + 0) * 8 + q) * 8 + g];
-            const int o = line * RP + nt * 8 + g;
             if (grp == 0) {
-              dmma(d[0], d[1], t0, Cq[o]);
-              if (STIFF) dmma(d[0], d[1], Ty[((ey * 2 + 1) * 8 + q) * 8 + g], Cq[TYP * RP + o]);
+              dmma(d[0], d[1], t0, Rb[o]);
+              if (STIFF) dmma(d[0], d[1], Ty[((ey * 2 + 1) * 8 + q) * 8 + g], Rb[CQL + o]);
             } else {
-              dmma(d[0], d[1], t0, Cq[2 * TYP * RP + o]);
+              dmma(d[0], d[1], t0, Rb[2 * CQL + o]);
             }
           }
-          double* srow = Sq + grp * LXR + (ey + g) * RP + nt * 8 + 2 * m;
+          double* srow = Sb + (ey + g) * RP + nt * 8 + 2 * m;
           srow[0] += d[0];
           srow[1] += d[1];
           __syncwarp();
@@ -472,8 +496,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     // last Z^T of the element, flush DoF layer e2 (complete for this chunk)
     for (int i = tid; i < FY * FX; i += NT) {
-      zt_item(e2, Q - 1, i);
-      int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
+      zt_item(e2, NB - 1, i);
+      const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
       double* yr = Yr + (e2 % P) * LXR + o;
       box[(int64_t)(e2 - z0) * FY * FX + i] = *yr;
       *yr = 0.0;
@@ -486,7 +510,7 @@ __global__ void __launch_bounds__(256, 1)
     const double* yr = Yr + (l % P) * LXR;
     double* dst = box + (int64_t)(l - z0) * FY * FX;
     for (int i = tid; i < FY * FX; i += NT) {
-      int n0 = i % FX, n1 = i / FX;
+      const int n0 = i % FX, n1 = i / FX;
       dst[i] = yr[n1 * RP + n0];
     }
   }
@@ -544,24 +568,25 @@ struct Launch {
   void (*kernel)(ApplyArgs, CUtensorMap);
 };
 
-template <int P, int Q, int EX, int EY, bool MASS, bool STIFF>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF>
 Launch make_launch() {
-  using C = Cfg<P, Q, EX, EY, MASS, STIFF>;
-  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, MASS, STIFF>};
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>;
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF>};
 }
 
-// Tile shapes per order (256 threads; EY·Q lines must be a multiple of 8).
+// Tile shapes per order: EY·Q lines in groups of 8, Q2B point layers per
+// batch, one warp per (point layer, line group) of a batch.
 template <bool MASS, bool STIFF>
 bool pick(int P, int Q, Launch* L) {
   if (P != Q) return false;
   switch (P) {
-    case 2: *L = make_launch<2, 2, 8, 4, MASS, STIFF>(); return true;
-    case 3: *L = make_launch<3, 3, 8, 8, MASS, STIFF>(); return true;
-    case 4: *L = make_launch<4, 4, 8, 4, MASS, STIFF>(); return true;
-    case 5: *L = make_launch<5, 5, 8, 8, MASS, STIFF>(); return true;
-    case 6: *L = make_launch<6, 6, 8, 4, MASS, STIFF>(); return true;
-    case 7: *L = make_launch<7, 7, 8, 8, MASS, STIFF>(); return true;
-    case 8: *L = make_launch<8, 8, 8, 4, MASS, STIFF>(); return true;
+    case 2: *L = make_launch<2, 2, 8, 8, 2, MASS, STIFF>(); return true;
+    case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF>(); return true;
+    case 4: *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>(); return true;
+    case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
+    case 6: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF>(); return true;
+    case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
+    case 8: *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF>(); return true;
     default: return false;
   }
 }
