@@ -46,7 +46,8 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, streamed every 50 ms while the
+    timed region runs (the recipe's clocks line, B200_PROFILING.md)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -55,30 +56,37 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
+        self._proc = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                parts = [p.strip() for p in out.strip().split(",")]
-                if len(parts) == 6:
-                    self.samples.append(parts)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _reader(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.strip().split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._reader, daemon=True)
+            self._t.start()
+            time.sleep(0.15)
+        except Exception:
+            self._proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._proc is not None:
+            time.sleep(0.1)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -98,34 +106,45 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_baseline(w, layers=None, seed=0):
-    """Time the oracle's slab-wise apply on a bounded sample of the workload."""
+def cpu_baseline(w, min_seconds=10.0, seed=0):
+    """Time the CPU oracle's slab-wise apply (oracle/igs_oracle.py apply_slab,
+    the numpy restatement of the reference algorithm) on a bounded sample:
+    one element layer of the last direction per task, all host cores, passes
+    repeated until `min_seconds` of work.  Coefficient values do not change
+    the work, so one layer of seeded planes is reused for every layer."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import igs_oracle as O
 
     d, p, K = w["d"], w["p"], w["K"]
     cores = os.cpu_count() or 1
-    layers = layers or min(K, max(4, cores))
     sp = [O.uniform_space(p, K) for _ in range(d)]
     ths = O.first_order_set(d)
     pm = O.plane_map(d, w["kind"])
-    shape = [p * K] * d
     n = int(np.prod([s.num_basis for s in sp]))
     x = O.recipe_x(n, seed)
-    # sample: element layers [0, layers) of the last direction, one slab per thread
-    planes = [O.synthetic_planes(d, shape, z * p, (z + 1) * p, w["kind"], seed) for z in range(layers)]
-    from concurrent.futures import ThreadPoolExecutor
+    layer_pts = (p * K) ** (d - 1) * p
+    nplanes = len({v for row in pm for v in row if v >= 0})
+    rng = np.random.default_rng(seed)
+    planes = 1.0 + 0.05 * rng.random((nplanes, layer_pts))
+    layers = min(K, cores)
 
     def one(z):
-        return O.apply_slab(sp, p, ths, ths, pm, planes[z], x, z, z + 1)
+        return O.apply_slab(sp, p, ths, ths, pm, planes, x, z, z + 1)
 
+    done = 0
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=cores) as ex:
-        list(ex.map(one, range(layers)))
+        while True:
+            list(ex.map(one, range(layers)))
+            done += layers
+            if time.perf_counter() - t0 >= min_seconds:
+                break
     t = time.perf_counter() - t0
-    frac = layers / K
+    frac = done / K
     return {"value": n * frac / t, "unit": "DoF/s", "cores": cores, "kind": "port",
-            "sample": f"{layers} of {K} element layers of one apply ({frac:.3f} of the work), "
-                      f"numpy oracle (oracle/igs_oracle.py apply_slab), {t:.2f} s"}
+            "sample": f"{done} element layers ({frac:.2f} applies' worth) of {w['desc']}, "
+                      f"numpy oracle apply_slab on {cores} threads, {t:.1f} s"}
 
 
 def run_reference(args, w):
@@ -135,7 +154,7 @@ def run_reference(args, w):
     steps = []
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(w, layers=min(w["K"], os.cpu_count() or 1))
+        cb = cpu_baseline(w, min_seconds=1.0 if i < args.warmup else min(5.0, 150.0 / max(1, args.steps)))
         if i >= args.warmup:
             steps.append(cb["value"])
     value = float(np.median(steps))
@@ -151,7 +170,7 @@ def run_reference(args, w):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -39,6 +39,9 @@ struct AsmPlan {
   int g_h[kMaxBlocks];          // stage-2 group (3D)
   int nh;                       // stage-2 groups (3D: keyed by v2)
   int h_v2[kMaxBlocks];
+  int npl;                      // distinct coefficient planes
+  int pl_list[kMaxBlocks];
+  int b_ps[kMaxBlocks];         // block -> index into pl_list
 };
 
 bool build_plan(const igs_problem* p, AsmPlan* plan) {
@@ -76,6 +79,14 @@ bool build_plan(const igs_problem* p, AsmPlan* plan) {
           P.g_h[g] = h;
         }
       }
+      int ps = -1;
+      for (int q = 0; q < P.npl; ++q)
+        if (P.pl_list[q] == pl) ps = q;
+      if (ps < 0) {
+        ps = P.npl++;
+        P.pl_list[ps] = pl;
+      }
+      P.b_ps[P.nb] = ps;
       P.b_plane[P.nb] = pl;
       P.b_v0[P.nb] = v[0];
       P.b_g[P.nb] = g;
@@ -116,89 +127,184 @@ struct Asm3Args {
   int nt0, nt1;       // row tiles
 };
 
+__device__ __forceinline__ void dmma_a(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Stage-1/2 tile plan: T x T rows in (x, y), their (T+P-1)-element support
+// region, slots = T·(2P-1) band entries per direction.
 template <int P, int Q, int T>
 struct A3Cfg {
   static constexpr int W = 2 * P - 1;        // band width
   static constexpr int PT = T * W;           // slots per tile per direction
+  static constexpr int PTP = (PT + 7) & ~7;  // padded to MMA tiles
   static constexpr int ER = T + P - 1;       // elements in the support region
   static constexpr int XR = ER * Q;          // points in the region
-  static constexpr int NT = 256;
+  static constexpr int XRP = (XR + 7) & ~7;  // padded to MMA tiles
+  static constexpr int NLP = P * P;          // element-local (n, m) pairs
+  static constexpr int NLT = (NLP + 7) / 8;  // ... in MMA tiles of 8
+  static constexpr int KS = (Q + 3) / 4;     // MMA k-steps per element (points)
+  static constexpr int QP = KS * 4;          // points per element, padded
+  static constexpr int NT = 256, NW = 8;
+  // shared memory (doubles)
+  static constexpr int WT = ER * 4 * QP * NLT * 8;  // W tables [e][v][q][pair] per direction
+  static constexpr size_t smem(int npl, int ng, int nh) {
+    size_t f = (size_t)npl * XRP * XR;                 // coefficient tile [plane][y][x]
+    size_t h = (size_t)nh * PTP * PTP;                 // H tile (aliases F)
+    size_t g = (size_t)ng * XRP * PTP;                 // G [g][y][s0]
+    return ((f > h ? f : h) + g + 2 * (size_t)WT) * sizeof(double);
+  }
 };
 
+// W^{v}[q][pair] of element e: w(q)·B^θ_{jn}(q)·B^η_{jm}(q), pair = jn·P + jm,
+// v = θ + 2η; zero for padded points/pairs and elements outside the mesh.
 template <int P, int Q, int T>
-__global__ void __launch_bounds__(256) asm3_stage12(const Asm3Args a) {
+__device__ void fill_wtab(double* Wt, const TabArgs& t, int dir, int64_t e_first) {
   using C = A3Cfg<P, Q, T>;
-  constexpr int W = C::W, PT = C::PT, XR = C::XR, NT = C::NT;
-  extern __shared__ double sm[];
+  for (int i = threadIdx.x; i < C::WT; i += C::NT) {
+    const int pr = i % (C::NLT * 8), q = (i / (C::NLT * 8)) % C::QP, v = (i / (C::NLT * 8 * C::QP)) % 4,
+              el = i / (C::NLT * 8 * C::QP * 4);
+    const int64_t e = e_first + el;
+    double val = 0.0;
+    if (pr < C::NLP && q < Q && e >= 0 && e < t.K[dir]) {
+      const int jn = pr / P, jm = pr % P, th = v & 1, et = v >> 1;
+      const int64_t x = e * Q + q;
+      if (th <= t.md[dir] && et <= t.md[dir]) {
+        const double w = t.wts[dir][x];
+        const double bn = t.vals[dir][((int64_t)th * P + jn) * t.X[dir] + x];
+        const double bm = t.vals[dir][((int64_t)et * P + jm) * t.X[dir] + x];
+        val = (w * bn) * bm;
+      }
+    }
+    Wt[i] = val;
+  }
+}
+
+// Per (point layer z, tile of T x T rows):
+//   stage 1 (x):  G_g[y][s0] = Σ_{b∈g} Σ_q F_b[y][e0·Q+q] · W0^{v0(b)}_{e0}[q][pair]   (DMMA, M=y N=pair K=q)
+//   stage 2 (y):  H_h[s1][s0] = Σ_{g∈h} Σ_q W1^{v1(g)}_{e1}[pair1][q] · G_g[e1·Q+q][s0] (DMMA, M=pair1 N=s0 K=q)
+// with the element-local pair results overlap-added into band slots by the
+// warp that owns those columns (no races, fixed order).
+template <int P, int Q, int T>
+__global__ void __launch_bounds__(256, 1) asm3_stage12(const Asm3Args a) {
+  using C = A3Cfg<P, Q, T>;
+  constexpr int W = C::W, PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, ER = C::ER;
+  constexpr int NLT = C::NLT, KS = C::KS, QP = C::QP, NT = C::NT, NW = C::NW;
+  extern __shared__ __align__(16) double sm[];
   const AsmPlan& pl = a.plan;
-  const int nb = pl.nb, ng = pl.ng, nh = pl.nh;
-  double* Fs = sm;                         // [nb-planes][XR(y)][XR(x)] (by block)
-  double* Gs = Fs + (size_t)nb * XR * XR;  // [ng][PT][XR(y)]
-  const int tid = threadIdx.x;
+  const int nb = pl.nb, ng = pl.ng, nh = pl.nh, npl = pl.npl;
+  const size_t fsz = (size_t)npl * XRP * XR, hsz = (size_t)nh * PTP * PTP;
+  double* Fs = sm;                                  // [npl][XRP y][XR x]
+  double* Hs = sm;                                  // [nh][PTP s1][PTP s0]   (after stage 1)
+  double* Gs = sm + (fsz > hsz ? fsz : hsz);        // [ng][XRP y][PTP s0]
+  double* W0 = Gs + (size_t)ng * XRP * PTP;         // [ER][4][QP][NLT*8]
+  double* W1 = W0 + C::WT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, m4 = lane & 3;
   const int t0 = blockIdx.x % a.nt0, t1 = blockIdx.x / a.nt0;
   const int64_t x2 = blockIdx.y;
-  const int a0 = t0 * T, a1 = t1 * T;           // first rows of the tile
-  const int64_t xb0 = (int64_t)(a0 - (P - 1)) * Q, xb1 = (int64_t)(a1 - (P - 1)) * Q;  // first region points
+  const int a0 = t0 * T, a1 = t1 * T;                     // first rows of the tile
+  const int64_t eb0 = a0 - (P - 1), eb1 = a1 - (P - 1);   // first region elements
+  const int64_t xb0 = eb0 * Q, xb1 = eb1 * Q;             // first region points
   const int64_t X0 = a.tab.X[0], X1 = a.tab.X[1];
-  // coefficient tile (distinct planes only once is not needed: F per block)
-  for (int i = tid; i < nb * XR * XR; i += NT) {
-    int b = i / (XR * XR), r = i % (XR * XR);
-    int yl = r / XR, xl = r % XR;
-    int64_t gx = xb0 + xl, gy = xb1 + yl;
+  for (int i = tid; i < npl * XRP * XR; i += NT) {
+    const int c = i / (XRP * XR), r = i % (XRP * XR), yl = r / XR, xl = r % XR;
+    const int64_t gx = xb0 + xl, gy = xb1 + yl;
     double v = 0.0;
-    if (gx >= 0 && gx < X0 && gy >= 0 && gy < X1)
-      v = __ldg(a.planes + (int64_t)pl.b_plane[b] * a.pstride + (x2 * X1 + gy) * X0 + gx);
+    if (yl < XR && gx >= 0 && gx < X0 && gy >= 0 && gy < X1)
+      v = __ldg(a.planes + (int64_t)pl.pl_list[c] * a.pstride + (x2 * X1 + gy) * X0 + gx);
     Fs[i] = v;
   }
+  for (int i = tid; i < ng * XRP * PTP; i += NT) Gs[i] = 0.0;
+  fill_wtab<P, Q, T>(W0, a.tab, 0, eb0);
+  fill_wtab<P, Q, T>(W1, a.tab, 1, eb1);
   __syncthreads();
-  // stage 1: G_g[s0][y] = Σ_b∈g Σ_x W0^{v0(b)}[pair0(s0)][x] F_b[y][x]
-  for (int i = tid; i < PT * XR; i += NT) {
-    const int s0 = i / XR, yl = i % XR;
-    const int64_t m0 = a0 + s0 / W, n0 = m0 + (s0 % W) - (P - 1);
-    double acc[kMaxBlocks];
-    for (int g = 0; g < ng; ++g) acc[g] = 0.0;
-    if (m0 < a.tab.N[0] && n0 >= 0 && n0 < a.tab.N[0]) {
-      int64_t elo = (m0 > n0 ? m0 : n0) - (P - 1), ehi = m0 < n0 ? m0 : n0;
-      if (elo < 0) elo = 0;
-      if (ehi > a.tab.K[0] - 1) ehi = a.tab.K[0] - 1;
-      for (int64_t e = elo; e <= ehi; ++e)
-        for (int q = 0; q < Q; ++q) {
-          const int64_t x = e * Q + q;
-          const double w = a.tab.wts[0][x];
-          const double bn0 = bval<P, Q>(a.tab, 0, 0, n0, x), bn1 = bval<P, Q>(a.tab, 0, 1, n0, x);
-          const double bm0 = bval<P, Q>(a.tab, 0, 0, m0, x), bm1 = bval<P, Q>(a.tab, 0, 1, m0, x);
-          const double wv[4] = {(w * bn0) * bm0, (w * bn1) * bm0, (w * bn0) * bm1, (w * bn1) * bm1};
-          const double* fcol = Fs + (int64_t)yl * XR + (x - xb0);
-          for (int b = 0; b < nb; ++b) acc[pl.b_g[b]] = fma(wv[pl.b_v0[b]], fcol[(int64_t)b * XR * XR], acc[pl.b_g[b]]);
+
+  // ---- stage 1: task = (group, y tile); sweep the region's elements ---------
+  for (int t = warp; t < ng * (XRP / 8); t += NW) {
+    const int g = t / (XRP / 8), yt = t % (XRP / 8);
+    const int y = yt * 8 + g8;  // A row
+    double* Gg = Gs + (size_t)g * XRP * PTP;
+    for (int el = 0; el < ER; ++el) {
+      double d[NLT][2];
+#pragma unroll
+      for (int nt = 0; nt < NLT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+      for (int b = 0; b < nb; ++b) {
+        if (pl.b_g[b] != g) continue;
+        const double* Fb = Fs + (size_t)pl.b_ps[b] * XRP * XR + (size_t)y * XR + el * Q;
+        const double* Wb = W0 + ((size_t)(el * 4 + pl.b_v0[b]) * QP) * (NLT * 8);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int q = ks * 4 + m4;
+          const double av = q < Q ? Fb[q] : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < NLT; ++nt) dmma_a(d[nt][0], d[nt][1], av, Wb[q * (NLT * 8) + nt * 8 + g8]);
         }
+      }
+      // overlap-add D[y][pair] into G[y][slot(m0, n0)] (rows m0 of the tile only)
+#pragma unroll
+      for (int nt = 0; nt < NLT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int pr = nt * 8 + 2 * m4 + c;
+          if (pr >= P * P) continue;
+          const int jn = pr / P, jm = pr % P;
+          const int64_t m0 = eb0 + el + jm, n0 = eb0 + el + jn;
+          if (m0 < a0 || m0 >= a0 + T || n0 < 0 || n0 >= a.tab.N[0] || m0 >= a.tab.N[0]) continue;
+          const int s0 = (int)(m0 - a0) * W + (jn - jm + P - 1);
+          Gg[(size_t)y * PTP + s0] += d[nt][c];
+        }
+      __syncwarp();
     }
-    for (int g = 0; g < ng; ++g) Gs[((int64_t)g * PT + s0) * XR + yl] = acc[g];
   }
   __syncthreads();
-  // stage 2: H_h[s1][s0] = Σ_{g∈h} Σ_y W1^{v1(g)}[pair1(s1)][y] G_g[s0][y]
-  for (int i = tid; i < PT * PT; i += NT) {
-    const int s1 = i / PT, s0 = i % PT;
-    const int64_t m1 = a1 + s1 / W, n1 = m1 + (s1 % W) - (P - 1);
+  for (int i = tid; i < nh * PTP * PTP; i += NT) Hs[i] = 0.0;
+  __syncthreads();
+
+  // ---- stage 2: task = (h, s0 tile); sweep the region's y elements -----------
+  for (int t = warp; t < nh * (PTP / 8); t += NW) {
+    const int h = t / (PTP / 8), st = t % (PTP / 8);
+    double* Hh = Hs + (size_t)h * PTP * PTP;
+    for (int el = 0; el < ER; ++el) {
+      double d[NLT][2];
+#pragma unroll
+      for (int mt = 0; mt < NLT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+      for (int g = 0; g < ng; ++g) {
+        if (pl.g_h[g] != h) continue;
+        const double* Gg = Gs + (size_t)g * XRP * PTP + (size_t)(el * Q) * PTP + st * 8 + g8;
+        const double* Wg = W1 + ((size_t)(el * 4 + pl.g_v1[g]) * QP) * (NLT * 8);
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int q = ks * 4 + m4;
+          const double bv = q < Q ? Gg[(size_t)q * PTP] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < NLT; ++mt) dmma_a(d[mt][0], d[mt][1], Wg[q * (NLT * 8) + mt * 8 + g8], bv);
+        }
+      }
+      // D[pair1][s0]: rows pair1 = mt*8 + g8, cols s0 = st*8 + 2m4 + c
+#pragma unroll
+      for (int mt = 0; mt < NLT; ++mt) {
+        const int pr = mt * 8 + g8;
+        if (pr >= P * P) continue;
+        const int jn = pr / P, jm = pr % P;
+        const int64_t m1 = eb1 + el + jm, n1 = eb1 + el + jn;
+        if (m1 < a1 || m1 >= a1 + T || n1 < 0 || n1 >= a.tab.N[1] || m1 >= a.tab.N[1]) continue;
+        const int s1 = (int)(m1 - a1) * W + (jn - jm + P - 1);
+        Hh[(size_t)s1 * PTP + st * 8 + 2 * m4] += d[mt][0];
+        Hh[(size_t)s1 * PTP + st * 8 + 2 * m4 + 1] += d[mt][1];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ---- write H[x2][h][s1][s0] for the tile's valid slots ---------------------
+  for (int i = tid; i < nh * PT * PT; i += NT) {
+    const int h = i / (PT * PT), r = i % (PT * PT), s1 = r / PT, s0 = r % PT;
     const int64_t gs0 = (int64_t)a0 * W + s0, gs1 = (int64_t)a1 * W + s1;
     if (gs0 >= a.NS0 || gs1 >= a.NS1) continue;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    if (m1 < a.tab.N[1] && n1 >= 0 && n1 < a.tab.N[1]) {
-      int64_t elo = (m1 > n1 ? m1 : n1) - (P - 1), ehi = m1 < n1 ? m1 : n1;
-      if (elo < 0) elo = 0;
-      if (ehi > a.tab.K[1] - 1) ehi = a.tab.K[1] - 1;
-      for (int64_t e = elo; e <= ehi; ++e)
-        for (int q = 0; q < Q; ++q) {
-          const int64_t y = e * Q + q;
-          const double w = a.tab.wts[1][y];
-          const double bn0 = bval<P, Q>(a.tab, 1, 0, n1, y), bn1 = bval<P, Q>(a.tab, 1, 1, n1, y);
-          const double bm0 = bval<P, Q>(a.tab, 1, 0, m1, y), bm1 = bval<P, Q>(a.tab, 1, 1, m1, y);
-          const double wv[4] = {(w * bn0) * bm0, (w * bn1) * bm0, (w * bn0) * bm1, (w * bn1) * bm1};
-          const int yl = (int)(y - xb1);
-          for (int g = 0; g < ng; ++g)
-            acc[pl.g_h[g]] = fma(wv[pl.g_v1[g]], Gs[((int64_t)g * PT + s0) * XR + yl], acc[pl.g_h[g]]);
-        }
-    }
-    for (int h = 0; h < nh; ++h) a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = acc[h];
+    a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = Hs[((size_t)h * PTP + s1) * PTP + s0];
   }
 }
 
@@ -451,6 +557,19 @@ __global__ void __launch_bounds__(128) asm2_stage2(const Asm2bArgs a) {
 
 // ---- host side ----------------------------------------------------------------
 
+constexpr int kTile = 4;
+
+size_t asm3_smem(int P, const AsmPlan& pl) {
+  switch (P) {
+    case 2: return A3Cfg<2, 2, kTile>::smem(pl.npl, pl.ng, pl.nh);
+    case 3: return A3Cfg<3, 3, kTile>::smem(pl.npl, pl.ng, pl.nh);
+    case 4: return A3Cfg<4, 4, kTile>::smem(pl.npl, pl.ng, pl.nh);
+    case 5: return A3Cfg<5, 5, kTile>::smem(pl.npl, pl.ng, pl.nh);
+    case 6: return A3Cfg<6, 6, kTile>::smem(pl.npl, pl.ng, pl.nh);
+    default: return ~size_t(0);
+  }
+}
+
 struct AsmShape {
   FusedShape fs;
   AsmPlan plan;
@@ -485,11 +604,7 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
         if (s.plan.b_v0[b] != 0) return false;
     }
   if (s.fs.p < 2 || s.fs.p > 6 || s.fs.k != s.fs.p) return false;
-  if (d == 3) {  // stage-1/2 tile must fit shared memory
-    const int W = 2 * s.fs.p - 1, XR = (4 + s.fs.p - 1) * s.fs.k, PT = 4 * W;
-    size_t smem = ((size_t)s.plan.nb * XR * XR + (size_t)s.plan.ng * PT * XR) * sizeof(double);
-    if (smem > 232448) return false;
-  }
+  if (d == 3 && asm3_smem(s.fs.p, s.plan) > 232448) return false;  // stage-1/2 tile must fit
   (void)D;
   if (out) *out = s;
   return true;
@@ -507,8 +622,6 @@ TabArgs tab_args(const igs_problem* p) {
   }
   return t;
 }
-
-constexpr int kTile = 4;
 
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
@@ -532,7 +645,7 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   a.NS1 = s.fs.nfn[1] * C::W;
   a.nt0 = (int)ceil_div(s.fs.nfn[0], kTile);
   a.nt1 = (int)ceil_div(s.fs.nfn[1], kTile);
-  size_t smem = ((size_t)s.plan.nb * C::XR * C::XR + (size_t)s.plan.ng * C::PT * C::XR) * sizeof(double);
+  size_t smem = C::smem(s.plan.npl, s.plan.ng, s.plan.nh);
   if (smem > 232448) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage12<P, Q, kTile>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
