@@ -22,6 +22,7 @@
 //         ring[m2][n2] += Σ_h W_z^{v2(h)} H_h  ->  CSR
 //   2D: asm2_stage1 (x) -> HBM, asm2_stage2 (y ring, chunked) -> CSR.
 #include "fused.cuh"
+#include "tma.cuh"
 
 namespace igs {
 namespace {
@@ -125,6 +126,8 @@ struct Asm3Args {
   double* H;          // [X2][nh][NS1][NS0]
   int64_t NS0, NS1;   // slot counts N·(2P-1)
   int nt0, nt1;       // row tiles
+  int lz;             // z point layers per CTA
+  int nplanes;        // planes in the TMA box (all planes of the field)
 };
 
 __device__ __forceinline__ void dmma_a(double& d0, double& d1, double a, double b) {
@@ -151,10 +154,10 @@ struct A3Cfg {
   // shared memory (doubles)
   static constexpr int WT = ER * 4 * QP * NLT * 8;  // W tables [e][v][q][pair] per direction
   static constexpr size_t smem(int npl, int ng, int nh) {
-    size_t f = (size_t)npl * XRP * XR;                 // coefficient tile [plane][y][x]
-    size_t h = (size_t)nh * PTP * PTP;                 // H tile (aliases F)
+    size_t f = ((size_t)npl * XRP * XR + 15) & ~size_t(15);  // coefficient tile [plane][y][x]
+    size_t h = (size_t)nh * PTP * PTP;                 // H tile
     size_t g = (size_t)ng * XRP * PTP;                 // G [g][y][s0]
-    return ((f > h ? f : h) + g + 2 * (size_t)WT) * sizeof(double);
+    return (f + h + g + 2 * (size_t)WT) * sizeof(double) + 16;
   }
 };
 
@@ -182,129 +185,139 @@ __device__ void fill_wtab(double* Wt, const TabArgs& t, int dir, int64_t e_first
   }
 }
 
-// Per (point layer z, tile of T x T rows):
+// Per (tile of T x T rows, chunk of z point layers), for every layer:
 //   stage 1 (x):  G_g[y][s0] = Σ_{b∈g} Σ_q F_b[y][e0·Q+q] · W0^{v0(b)}_{e0}[q][pair]   (DMMA, M=y N=pair K=q)
 //   stage 2 (y):  H_h[s1][s0] = Σ_{g∈h} Σ_q W1^{v1(g)}_{e1}[pair1][q] · G_g[e1·Q+q][s0] (DMMA, M=pair1 N=s0 K=q)
 // with the element-local pair results overlap-added into band slots by the
-// warp that owns those columns (no races, fixed order).
+// warp that owns those columns (no races, fixed order).  The coefficient
+// region of the next layer is fetched by TMA while stage 2 runs.
 template <int P, int Q, int T>
-__global__ void __launch_bounds__(256, 1) asm3_stage12(const Asm3Args a) {
+__global__ void __launch_bounds__(256, 1)
+    asm3_stage12(const Asm3Args a, const __grid_constant__ CUtensorMap fmap) {
   using C = A3Cfg<P, Q, T>;
   constexpr int W = C::W, PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, ER = C::ER;
   constexpr int NLT = C::NLT, KS = C::KS, QP = C::QP, NT = C::NT, NW = C::NW;
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
-  const int nb = pl.nb, ng = pl.ng, nh = pl.nh, npl = pl.npl;
-  const size_t fsz = (size_t)npl * XRP * XR, hsz = (size_t)nh * PTP * PTP;
-  double* Fs = sm;                                  // [npl][XRP y][XR x]
-  double* Hs = sm;                                  // [nh][PTP s1][PTP s0]   (after stage 1)
-  double* Gs = sm + (fsz > hsz ? fsz : hsz);        // [ng][XRP y][PTP s0]
+  const int nb = pl.nb, ng = pl.ng, nh = pl.nh;
+  const size_t fsz = (size_t)a.nplanes * XRP * XR;
+  double* Fs = sm;                                  // [n_planes][XRP y][XR x]   (TMA box)
+  double* Hs = Fs + ((fsz + 15) & ~size_t(15));     // [nh][PTP s1][PTP s0]
+  double* Gs = Hs + (size_t)nh * PTP * PTP;         // [ng][XRP y][PTP s0]
   double* W0 = Gs + (size_t)ng * XRP * PTP;         // [ER][4][QP][NLT*8]
   double* W1 = W0 + C::WT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(W1 + C::WT);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, m4 = lane & 3;
   const int t0 = blockIdx.x % a.nt0, t1 = blockIdx.x / a.nt0;
-  const int64_t x2 = blockIdx.y;
+  const int64_t z_lo = (int64_t)blockIdx.y * a.lz;
+  const int64_t z_hi = min64(a.tab.X[2], z_lo + a.lz);
   const int a0 = t0 * T, a1 = t1 * T;                     // first rows of the tile
   const int64_t eb0 = a0 - (P - 1), eb1 = a1 - (P - 1);   // first region elements
-  const int64_t xb0 = eb0 * Q, xb1 = eb1 * Q;             // first region points
-  const int64_t X0 = a.tab.X[0], X1 = a.tab.X[1];
-  for (int i = tid; i < npl * XRP * XR; i += NT) {
-    const int c = i / (XRP * XR), r = i % (XRP * XR), yl = r / XR, xl = r % XR;
-    const int64_t gx = xb0 + xl, gy = xb1 + yl;
-    double v = 0.0;
-    if (yl < XR && gx >= 0 && gx < X0 && gy >= 0 && gy < X1)
-      v = __ldg(a.planes + (int64_t)pl.pl_list[c] * a.pstride + (x2 * X1 + gy) * X0 + gx);
-    Fs[i] = v;
+  const int xb0 = (int)eb0 * Q, xb1 = (int)eb1 * Q;       // first region points (may be < 0)
+  const unsigned fbytes = (unsigned)(fsz * sizeof(double));
+  if (tid == 0) {
+    dev::mbar_init(bar, 1);
+    dev::fence_mbar_init();
   }
-  for (int i = tid; i < ng * XRP * PTP; i += NT) Gs[i] = 0.0;
+  __syncthreads();
+  if (tid == 0) {
+    dev::mbar_expect_tx(bar, fbytes);
+    dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)z_lo, 0);
+  }
   fill_wtab<P, Q, T>(W0, a.tab, 0, eb0);
   fill_wtab<P, Q, T>(W1, a.tab, 1, eb1);
-  __syncthreads();
-
-  // ---- stage 1: task = (group, y tile); sweep the region's elements ---------
-  for (int t = warp; t < ng * (XRP / 8); t += NW) {
-    const int g = t / (XRP / 8), yt = t % (XRP / 8);
-    const int y = yt * 8 + g8;  // A row
-    double* Gg = Gs + (size_t)g * XRP * PTP;
-    for (int el = 0; el < ER; ++el) {
-      double d[NLT][2];
+  unsigned phase = 0;
+  for (int64_t x2 = z_lo; x2 < z_hi; ++x2, phase ^= 1) {
+    for (int i = tid; i < ng * XRP * PTP; i += NT) Gs[i] = 0.0;
+    __syncthreads();
+    dev::mbar_wait(bar, phase);
+    // ---- stage 1: task = (group, y tile); sweep the region's elements -------
+    for (int t = warp; t < ng * (XRP / 8); t += NW) {
+      const int g = t / (XRP / 8), yt = t % (XRP / 8);
+      const int y = yt * 8 + g8;  // A row
+      double* Gg = Gs + (size_t)g * XRP * PTP;
+      for (int el = 0; el < ER; ++el) {
+        double d[NLT][2];
 #pragma unroll
-      for (int nt = 0; nt < NLT; ++nt) d[nt][0] = d[nt][1] = 0.0;
-      for (int b = 0; b < nb; ++b) {
-        if (pl.b_g[b] != g) continue;
-        const double* Fb = Fs + (size_t)pl.b_ps[b] * XRP * XR + (size_t)y * XR + el * Q;
-        const double* Wb = W0 + ((size_t)(el * 4 + pl.b_v0[b]) * QP) * (NLT * 8);
+        for (int nt = 0; nt < NLT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+        for (int b = 0; b < nb; ++b) {
+          if (pl.b_g[b] != g) continue;
+          const double* Fb = Fs + (size_t)pl.b_plane[b] * XRP * XR + (size_t)y * XR + el * Q;
+          const double* Wb = W0 + ((size_t)(el * 4 + pl.b_v0[b]) * QP) * (NLT * 8);
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int q = ks * 4 + m4;
-          const double av = q < Q ? Fb[q] : 0.0;
+          for (int ks = 0; ks < KS; ++ks) {
+            const int q = ks * 4 + m4;
+            const double av = q < Q ? Fb[q] : 0.0;
 #pragma unroll
-          for (int nt = 0; nt < NLT; ++nt) dmma_a(d[nt][0], d[nt][1], av, Wb[q * (NLT * 8) + nt * 8 + g8]);
+            for (int nt = 0; nt < NLT; ++nt) dmma_a(d[nt][0], d[nt][1], av, Wb[q * (NLT * 8) + nt * 8 + g8]);
+          }
         }
+#pragma unroll
+        for (int nt = 0; nt < NLT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int pr = nt * 8 + 2 * m4 + c;
+            if (pr >= P * P) continue;
+            const int jn = pr / P, jm = pr % P;
+            const int64_t m0 = eb0 + el + jm, n0 = eb0 + el + jn;
+            if (m0 < a0 || m0 >= a0 + T || n0 < 0 || n0 >= a.tab.N[0] || m0 >= a.tab.N[0]) continue;
+            const int s0 = (int)(m0 - a0) * W + (jn - jm + P - 1);
+            Gg[(size_t)y * PTP + s0] += d[nt][c];
+          }
+        __syncwarp();
       }
-      // overlap-add D[y][pair] into G[y][slot(m0, n0)] (rows m0 of the tile only)
+    }
+    for (int i = tid; i < nh * PTP * PTP; i += NT) Hs[i] = 0.0;
+    __syncthreads();
+    // F is consumed: fetch the next layer's region while stage 2 runs
+    if (tid == 0 && x2 + 1 < z_hi) {
+      dev::fence_proxy_async();
+      dev::mbar_expect_tx(bar, fbytes);
+      dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)(x2 + 1), 0);
+    }
+    // ---- stage 2: task = (h, s0 tile); sweep the region's y elements ---------
+    for (int t = warp; t < nh * (PTP / 8); t += NW) {
+      const int h = t / (PTP / 8), st = t % (PTP / 8);
+      double* Hh = Hs + (size_t)h * PTP * PTP;
+      for (int el = 0; el < ER; ++el) {
+        double d[NLT][2];
 #pragma unroll
-      for (int nt = 0; nt < NLT; ++nt)
+        for (int mt = 0; mt < NLT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+        for (int g = 0; g < ng; ++g) {
+          if (pl.g_h[g] != h) continue;
+          const double* Gg = Gs + (size_t)g * XRP * PTP + (size_t)(el * Q) * PTP + st * 8 + g8;
+          const double* Wg = W1 + ((size_t)(el * 4 + pl.g_v1[g]) * QP) * (NLT * 8);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int pr = nt * 8 + 2 * m4 + c;
+          for (int ks = 0; ks < KS; ++ks) {
+            const int q = ks * 4 + m4;
+            const double bv = q < Q ? Gg[(size_t)q * PTP] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < NLT; ++mt) dmma_a(d[mt][0], d[mt][1], Wg[q * (NLT * 8) + mt * 8 + g8], bv);
+          }
+        }
+#pragma unroll
+        for (int mt = 0; mt < NLT; ++mt) {
+          const int pr = mt * 8 + g8;
           if (pr >= P * P) continue;
           const int jn = pr / P, jm = pr % P;
-          const int64_t m0 = eb0 + el + jm, n0 = eb0 + el + jn;
-          if (m0 < a0 || m0 >= a0 + T || n0 < 0 || n0 >= a.tab.N[0] || m0 >= a.tab.N[0]) continue;
-          const int s0 = (int)(m0 - a0) * W + (jn - jm + P - 1);
-          Gg[(size_t)y * PTP + s0] += d[nt][c];
+          const int64_t m1 = eb1 + el + jm, n1 = eb1 + el + jn;
+          if (m1 < a1 || m1 >= a1 + T || n1 < 0 || n1 >= a.tab.N[1] || m1 >= a.tab.N[1]) continue;
+          const int s1 = (int)(m1 - a1) * W + (jn - jm + P - 1);
+          Hh[(size_t)s1 * PTP + st * 8 + 2 * m4] += d[mt][0];
+          Hh[(size_t)s1 * PTP + st * 8 + 2 * m4 + 1] += d[mt][1];
         }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < nh * PTP * PTP; i += NT) Hs[i] = 0.0;
-  __syncthreads();
-
-  // ---- stage 2: task = (h, s0 tile); sweep the region's y elements -----------
-  for (int t = warp; t < nh * (PTP / 8); t += NW) {
-    const int h = t / (PTP / 8), st = t % (PTP / 8);
-    double* Hh = Hs + (size_t)h * PTP * PTP;
-    for (int el = 0; el < ER; ++el) {
-      double d[NLT][2];
-#pragma unroll
-      for (int mt = 0; mt < NLT; ++mt) d[mt][0] = d[mt][1] = 0.0;
-      for (int g = 0; g < ng; ++g) {
-        if (pl.g_h[g] != h) continue;
-        const double* Gg = Gs + (size_t)g * XRP * PTP + (size_t)(el * Q) * PTP + st * 8 + g8;
-        const double* Wg = W1 + ((size_t)(el * 4 + pl.g_v1[g]) * QP) * (NLT * 8);
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int q = ks * 4 + m4;
-          const double bv = q < Q ? Gg[(size_t)q * PTP] : 0.0;
-#pragma unroll
-          for (int mt = 0; mt < NLT; ++mt) dmma_a(d[mt][0], d[mt][1], Wg[q * (NLT * 8) + mt * 8 + g8], bv);
-        }
+        __syncwarp();
       }
-      // D[pair1][s0]: rows pair1 = mt*8 + g8, cols s0 = st*8 + 2m4 + c
-#pragma unroll
-      for (int mt = 0; mt < NLT; ++mt) {
-        const int pr = mt * 8 + g8;
-        if (pr >= P * P) continue;
-        const int jn = pr / P, jm = pr % P;
-        const int64_t m1 = eb1 + el + jm, n1 = eb1 + el + jn;
-        if (m1 < a1 || m1 >= a1 + T || n1 < 0 || n1 >= a.tab.N[1] || m1 >= a.tab.N[1]) continue;
-        const int s1 = (int)(m1 - a1) * W + (jn - jm + P - 1);
-        Hh[(size_t)s1 * PTP + st * 8 + 2 * m4] += d[mt][0];
-        Hh[(size_t)s1 * PTP + st * 8 + 2 * m4 + 1] += d[mt][1];
-      }
-      __syncwarp();
     }
-  }
-  __syncthreads();
-  // ---- write H[x2][h][s1][s0] for the tile's valid slots ---------------------
-  for (int i = tid; i < nh * PT * PT; i += NT) {
-    const int h = i / (PT * PT), r = i % (PT * PT), s1 = r / PT, s0 = r % PT;
-    const int64_t gs0 = (int64_t)a0 * W + s0, gs1 = (int64_t)a1 * W + s1;
-    if (gs0 >= a.NS0 || gs1 >= a.NS1) continue;
-    a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = Hs[((size_t)h * PTP + s1) * PTP + s0];
+    __syncthreads();
+    // ---- write H[x2][h][s1][s0] for the tile's valid slots -------------------
+    for (int i = tid; i < nh * PT * PT; i += NT) {
+      const int h = i / (PT * PT), r = i % (PT * PT), s1 = r / PT, s0 = r % PT;
+      const int64_t gs0 = (int64_t)a0 * W + s0, gs1 = (int64_t)a1 * W + s1;
+      if (gs0 >= a.NS0 || gs1 >= a.NS1) continue;
+      a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = Hs[((size_t)h * PTP + s1) * PTP + s0];
+    }
   }
 }
 
@@ -559,13 +572,13 @@ __global__ void __launch_bounds__(128) asm2_stage2(const Asm2bArgs a) {
 
 constexpr int kTile = 4;
 
-size_t asm3_smem(int P, const AsmPlan& pl) {
+size_t asm3_smem(int P, const AsmPlan& pl, int nplanes) {
   switch (P) {
-    case 2: return A3Cfg<2, 2, kTile>::smem(pl.npl, pl.ng, pl.nh);
-    case 3: return A3Cfg<3, 3, kTile>::smem(pl.npl, pl.ng, pl.nh);
-    case 4: return A3Cfg<4, 4, kTile>::smem(pl.npl, pl.ng, pl.nh);
-    case 5: return A3Cfg<5, 5, kTile>::smem(pl.npl, pl.ng, pl.nh);
-    case 6: return A3Cfg<6, 6, kTile>::smem(pl.npl, pl.ng, pl.nh);
+    case 2: return A3Cfg<2, 2, kTile>::smem(nplanes, pl.ng, pl.nh);
+    case 3: return A3Cfg<3, 3, kTile>::smem(nplanes, pl.ng, pl.nh);
+    case 4: return A3Cfg<4, 4, kTile>::smem(nplanes, pl.ng, pl.nh);
+    case 5: return A3Cfg<5, 5, kTile>::smem(nplanes, pl.ng, pl.nh);
+    case 6: return A3Cfg<6, 6, kTile>::smem(nplanes, pl.ng, pl.nh);
     default: return ~size_t(0);
   }
 }
@@ -604,7 +617,11 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
         if (s.plan.b_v0[b] != 0) return false;
     }
   if (s.fs.p < 2 || s.fs.p > 6 || s.fs.k != s.fs.p) return false;
-  if (d == 3 && asm3_smem(s.fs.p, s.plan) > 232448) return false;  // stage-1/2 tile must fit
+  if (d == 3) {
+    if (asm3_smem(s.fs.p, s.plan, p->n_planes) > 232448) return false;  // stage-1/2 tile must fit
+    // TMA: 16-byte aligned rows and plane stride
+    if ((s.fs.npt[0] * 8) % 16 != 0 || (p->plane_stride * 8) % 16 != 0 || p->n_planes > 256) return false;
+  }
   (void)D;
   if (out) *out = s;
   return true;
@@ -645,13 +662,27 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   a.NS1 = s.fs.nfn[1] * C::W;
   a.nt0 = (int)ceil_div(s.fs.nfn[0], kTile);
   a.nt1 = (int)ceil_div(s.fs.nfn[1], kTile);
-  size_t smem = C::smem(s.plan.npl, s.plan.ng, s.plan.nh);
+  a.nplanes = p->n_planes;
+  size_t smem = C::smem(a.nplanes, s.plan.ng, s.plan.nh);
   if (smem > 232448) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
+  if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
+  CUtensorMap fmap;
+  {
+    const int64_t dims[4] = {s.fs.npt[0], s.fs.npt[1], s.fs.npt[2], p->n_planes};
+    const unsigned box[4] = {(unsigned)C::XR, (unsigned)C::XRP, 1u, (unsigned)p->n_planes};
+    IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
+  }
+  // z chunks: enough CTAs for ~4 waves at one CTA per SM
+  const int64_t tiles = (int64_t)a.nt0 * a.nt1;
+  int64_t nz = ceil_div(148 * 4, tiles);
+  if (nz < 1) nz = 1;
+  a.lz = (int)ceil_div(s.fs.npt[2], nz);
+  if (a.lz < 1) a.lz = 1;
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage12<P, Q, kTile>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                      "smem attribute"));
-  dim3 grid((unsigned)(a.nt0 * a.nt1), (unsigned)s.fs.npt[2]);
-  asm3_stage12<P, Q, kTile><<<grid, C::NT, smem, st>>>(a);
+  dim3 grid((unsigned)tiles, (unsigned)ceil_div(s.fs.npt[2], a.lz));
+  asm3_stage12<P, Q, kTile><<<grid, C::NT, smem, st>>>(a, fmap);
   IGS_LAUNCH_CHECK("asm3_stage12");
   Asm3bArgs b{};
   b.plan = s.plan;

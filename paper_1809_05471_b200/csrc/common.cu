@@ -140,3 +140,32 @@ extern "C" igs_status igs_layers_copy(const double* src, double* dst, int64_t co
   IGS_LAUNCH_CHECK("layers_copy_kernel");
   return IGS_OK;
 }
+
+// ---- TMA tensor maps over coefficient planes ---------------------------------
+#include "tma.cuh"
+
+namespace igs {
+
+igs_status planes_tensor_map(CUtensorMap* map, const double* planes, const int64_t dims[4],
+                             int64_t pstride, const unsigned box[4]) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(IGS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t gd[4] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2], (cuuint64_t)dims[3]};
+  cuuint64_t gs[3] = {(cuuint64_t)dims[0] * 8, (cuuint64_t)(dims[0] * dims[1]) * 8, (cuuint64_t)pstride * 8};
+  cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(planes), gd, gs, bd, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(IGS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return IGS_OK;
+}
+
+}  // namespace igs
