@@ -43,6 +43,8 @@ struct AsmPlan {
   int npl;                      // distinct coefficient planes
   int pl_list[kMaxBlocks];
   int b_ps[kMaxBlocks];         // block -> index into pl_list
+  int g_b0[kMaxBlocks], g_nb[kMaxBlocks];  // blocks of group g: [g_b0, g_b0 + g_nb)
+  int h_g0[kMaxBlocks], h_ng[kMaxBlocks];  // groups of stage-2 group h (3D)
 };
 
 bool build_plan(const igs_problem* p, AsmPlan* plan) {
@@ -94,7 +96,38 @@ bool build_plan(const igs_problem* p, AsmPlan* plan) {
       ++P.nb;
     }
   if (P.nb == 0) return false;
-  *plan = P;
+  // Renumber groups so each stage-2 group's groups are contiguous, then order
+  // blocks by group (stable: the reference's block order within a group).
+  int gperm[kMaxBlocks], ng_new = 0;
+  if (d == 3) {
+    for (int h = 0; h < P.nh; ++h) {
+      P.h_g0[h] = ng_new;
+      for (int g = 0; g < P.ng; ++g)
+        if (P.g_h[g] == h) gperm[g] = ng_new++;
+      P.h_ng[h] = ng_new - P.h_g0[h];
+    }
+  } else {
+    for (int g = 0; g < P.ng; ++g) gperm[g] = g;
+  }
+  AsmPlan Q = P;
+  for (int g = 0; g < P.ng; ++g) {
+    Q.g_v1[gperm[g]] = P.g_v1[g];
+    Q.g_h[gperm[g]] = P.g_h[g];
+  }
+  int nbo = 0;
+  for (int gn = 0; gn < P.ng; ++gn) {
+    Q.g_b0[gn] = nbo;
+    for (int b = 0; b < P.nb; ++b)
+      if (gperm[P.b_g[b]] == gn) {
+        Q.b_plane[nbo] = P.b_plane[b];
+        Q.b_v0[nbo] = P.b_v0[b];
+        Q.b_ps[nbo] = P.b_ps[b];
+        Q.b_g[nbo] = gn;
+        ++nbo;
+      }
+    Q.g_nb[gn] = nbo - Q.g_b0[gn];
+  }
+  *plan = Q;
   return true;
 }
 
@@ -150,13 +183,17 @@ struct A3Cfg {
   static constexpr int NLT = (NLP + 7) / 8;  // ... in MMA tiles of 8
   static constexpr int KS = (Q + 3) / 4;     // MMA k-steps per element (points)
   static constexpr int QP = KS * 4;          // points per element, padded
-  static constexpr int NT = 256, NW = 8;
+  static constexpr int NT = 512, NW = 16;
+  // Row pitches ≡ 8 (mod 16) doubles: the MMA fragment loads that walk 4
+  // rows x 8 consecutive doubles then hit every bank exactly twice.
+  static constexpr int WP = ((NLT * 8 + 7) / 16) * 16 + 8;  // W-table row (pairs)
+  static constexpr int GP = ((PTP + 7) / 16) * 16 + 8;      // G / H row (slots)
   // shared memory (doubles)
-  static constexpr int WT = ER * 4 * QP * NLT * 8;  // W tables [e][v][q][pair] per direction
+  static constexpr int WT = ER * 4 * QP * WP;  // W tables [e][v][q][pair] per direction
   static constexpr size_t smem(int npl, int ng, int nh) {
     size_t f = ((size_t)npl * XRP * XR + 15) & ~size_t(15);  // coefficient tile [plane][y][x]
-    size_t h = (size_t)nh * PTP * PTP;                 // H tile
-    size_t g = (size_t)ng * XRP * PTP;                 // G [g][y][s0]
+    size_t h = (size_t)nh * PTP * GP;                  // H tile [h][s1][s0]
+    size_t g = (size_t)ng * XRP * GP;                  // G [g][y][s0]
     return (f + h + g + 2 * (size_t)WT) * sizeof(double) + 16;
   }
 };
@@ -167,8 +204,8 @@ template <int P, int Q, int T>
 __device__ void fill_wtab(double* Wt, const TabArgs& t, int dir, int64_t e_first) {
   using C = A3Cfg<P, Q, T>;
   for (int i = threadIdx.x; i < C::WT; i += C::NT) {
-    const int pr = i % (C::NLT * 8), q = (i / (C::NLT * 8)) % C::QP, v = (i / (C::NLT * 8 * C::QP)) % 4,
-              el = i / (C::NLT * 8 * C::QP * 4);
+    const int pr = i % C::WP, q = (i / C::WP) % C::QP, v = (i / (C::WP * C::QP)) % 4,
+              el = i / (C::WP * C::QP * 4);
     const int64_t e = e_first + el;
     double val = 0.0;
     if (pr < C::NLP && q < Q && e >= 0 && e < t.K[dir]) {
@@ -192,23 +229,25 @@ __device__ void fill_wtab(double* Wt, const TabArgs& t, int dir, int64_t e_first
 // warp that owns those columns (no races, fixed order).  The coefficient
 // region of the next layer is fetched by TMA while stage 2 runs.
 template <int P, int Q, int T>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(512, 1)
     asm3_stage12(const Asm3Args a, const __grid_constant__ CUtensorMap fmap) {
   using C = A3Cfg<P, Q, T>;
   constexpr int W = C::W, PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, ER = C::ER;
   constexpr int NLT = C::NLT, KS = C::KS, QP = C::QP, NT = C::NT, NW = C::NW;
+  constexpr int WP = C::WP, GP = C::GP;
   extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
   const int nb = pl.nb, ng = pl.ng, nh = pl.nh;
   const size_t fsz = (size_t)a.nplanes * XRP * XR;
   double* Fs = sm;                                  // [n_planes][XRP y][XR x]   (TMA box)
-  double* Hs = Fs + ((fsz + 15) & ~size_t(15));     // [nh][PTP s1][PTP s0]
-  double* Gs = Hs + (size_t)nh * PTP * PTP;         // [ng][XRP y][PTP s0]
-  double* W0 = Gs + (size_t)ng * XRP * PTP;         // [ER][4][QP][NLT*8]
+  double* Hs = Fs + ((fsz + 15) & ~size_t(15));     // [nh][PTP s1][GP]
+  double* Gs = Hs + (size_t)nh * PTP * GP;          // [ng][XRP y][GP]
+  double* W0 = Gs + (size_t)ng * XRP * GP;          // [ER][4][QP][WP]
   double* W1 = W0 + C::WT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(W1 + C::WT);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, m4 = lane & 3;
+  const int N0 = (int)a.tab.N[0], N1 = (int)a.tab.N[1];
   const int t0 = blockIdx.x % a.nt0, t1 = blockIdx.x / a.nt0;
   const int64_t z_lo = (int64_t)blockIdx.y * a.lz;
   const int64_t z_hi = min64(a.tab.X[2], z_lo + a.lz);
@@ -229,28 +268,28 @@ __global__ void __launch_bounds__(256, 1)
   fill_wtab<P, Q, T>(W1, a.tab, 1, eb1);
   unsigned phase = 0;
   for (int64_t x2 = z_lo; x2 < z_hi; ++x2, phase ^= 1) {
-    for (int i = tid; i < ng * XRP * PTP; i += NT) Gs[i] = 0.0;
+    for (int i = tid; i < ng * XRP * GP; i += NT) Gs[i] = 0.0;
     __syncthreads();
     dev::mbar_wait(bar, phase);
     // ---- stage 1: task = (group, y tile); sweep the region's elements -------
     for (int t = warp; t < ng * (XRP / 8); t += NW) {
       const int g = t / (XRP / 8), yt = t % (XRP / 8);
       const int y = yt * 8 + g8;  // A row
-      double* Gg = Gs + (size_t)g * XRP * PTP;
+      double* Gg = Gs + g * XRP * GP;
+      const int b_lo = pl.g_b0[g], b_hi = b_lo + pl.g_nb[g];
       for (int el = 0; el < ER; ++el) {
         double d[NLT][2];
 #pragma unroll
         for (int nt = 0; nt < NLT; ++nt) d[nt][0] = d[nt][1] = 0.0;
-        for (int b = 0; b < nb; ++b) {
-          if (pl.b_g[b] != g) continue;
-          const double* Fb = Fs + (size_t)pl.b_plane[b] * XRP * XR + (size_t)y * XR + el * Q;
-          const double* Wb = W0 + ((size_t)(el * 4 + pl.b_v0[b]) * QP) * (NLT * 8);
+        for (int b = b_lo; b < b_hi; ++b) {
+          const double* Fb = Fs + pl.b_plane[b] * (XRP * XR) + y * XR + el * Q;
+          const double* Wb = W0 + (el * 4 + pl.b_v0[b]) * (QP * WP);
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int q = ks * 4 + m4;
             const double av = q < Q ? Fb[q] : 0.0;
 #pragma unroll
-            for (int nt = 0; nt < NLT; ++nt) dmma_a(d[nt][0], d[nt][1], av, Wb[q * (NLT * 8) + nt * 8 + g8]);
+            for (int nt = 0; nt < NLT; ++nt) dmma_a(d[nt][0], d[nt][1], av, Wb[q * WP + nt * 8 + g8]);
           }
         }
 #pragma unroll
@@ -260,15 +299,15 @@ __global__ void __launch_bounds__(256, 1)
             const int pr = nt * 8 + 2 * m4 + c;
             if (pr >= P * P) continue;
             const int jn = pr / P, jm = pr % P;
-            const int64_t m0 = eb0 + el + jm, n0 = eb0 + el + jn;
-            if (m0 < a0 || m0 >= a0 + T || n0 < 0 || n0 >= a.tab.N[0] || m0 >= a.tab.N[0]) continue;
-            const int s0 = (int)(m0 - a0) * W + (jn - jm + P - 1);
-            Gg[(size_t)y * PTP + s0] += d[nt][c];
+            const int m0 = (int)eb0 + el + jm, n0 = (int)eb0 + el + jn;
+            if (m0 < a0 || m0 >= a0 + T || n0 < 0 || n0 >= N0 || m0 >= N0) continue;
+            const int s0 = (m0 - a0) * W + (jn - jm + P - 1);
+            Gg[y * GP + s0] += d[nt][c];
           }
         __syncwarp();
       }
     }
-    for (int i = tid; i < nh * PTP * PTP; i += NT) Hs[i] = 0.0;
+    for (int i = tid; i < nh * PTP * GP; i += NT) Hs[i] = 0.0;
     __syncthreads();
     // F is consumed: fetch the next layer's region while stage 2 runs
     if (tid == 0 && x2 + 1 < z_hi) {
@@ -279,21 +318,21 @@ __global__ void __launch_bounds__(256, 1)
     // ---- stage 2: task = (h, s0 tile); sweep the region's y elements ---------
     for (int t = warp; t < nh * (PTP / 8); t += NW) {
       const int h = t / (PTP / 8), st = t % (PTP / 8);
-      double* Hh = Hs + (size_t)h * PTP * PTP;
+      double* Hh = Hs + h * PTP * GP;
+      const int g_lo = pl.h_g0[h], g_hi = g_lo + pl.h_ng[h];
       for (int el = 0; el < ER; ++el) {
         double d[NLT][2];
 #pragma unroll
         for (int mt = 0; mt < NLT; ++mt) d[mt][0] = d[mt][1] = 0.0;
-        for (int g = 0; g < ng; ++g) {
-          if (pl.g_h[g] != h) continue;
-          const double* Gg = Gs + (size_t)g * XRP * PTP + (size_t)(el * Q) * PTP + st * 8 + g8;
-          const double* Wg = W1 + ((size_t)(el * 4 + pl.g_v1[g]) * QP) * (NLT * 8);
+        for (int g = g_lo; g < g_hi; ++g) {
+          const double* Gg = Gs + g * XRP * GP + (el * Q) * GP + st * 8 + g8;
+          const double* Wg = W1 + (el * 4 + pl.g_v1[g]) * (QP * WP);
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int q = ks * 4 + m4;
-            const double bv = q < Q ? Gg[(size_t)q * PTP] : 0.0;
+            const double bv = q < Q ? Gg[q * GP] : 0.0;
 #pragma unroll
-            for (int mt = 0; mt < NLT; ++mt) dmma_a(d[mt][0], d[mt][1], Wg[q * (NLT * 8) + mt * 8 + g8], bv);
+            for (int mt = 0; mt < NLT; ++mt) dmma_a(d[mt][0], d[mt][1], Wg[q * WP + mt * 8 + g8], bv);
           }
         }
 #pragma unroll
@@ -301,11 +340,11 @@ __global__ void __launch_bounds__(256, 1)
           const int pr = mt * 8 + g8;
           if (pr >= P * P) continue;
           const int jn = pr / P, jm = pr % P;
-          const int64_t m1 = eb1 + el + jm, n1 = eb1 + el + jn;
-          if (m1 < a1 || m1 >= a1 + T || n1 < 0 || n1 >= a.tab.N[1] || m1 >= a.tab.N[1]) continue;
-          const int s1 = (int)(m1 - a1) * W + (jn - jm + P - 1);
-          Hh[(size_t)s1 * PTP + st * 8 + 2 * m4] += d[mt][0];
-          Hh[(size_t)s1 * PTP + st * 8 + 2 * m4 + 1] += d[mt][1];
+          const int m1 = (int)eb1 + el + jm, n1 = (int)eb1 + el + jn;
+          if (m1 < a1 || m1 >= a1 + T || n1 < 0 || n1 >= N1 || m1 >= N1) continue;
+          const int s1 = (m1 - a1) * W + (jn - jm + P - 1);
+          Hh[s1 * GP + st * 8 + 2 * m4] += d[mt][0];
+          Hh[s1 * GP + st * 8 + 2 * m4 + 1] += d[mt][1];
         }
         __syncwarp();
       }
@@ -316,7 +355,7 @@ __global__ void __launch_bounds__(256, 1)
       const int h = i / (PT * PT), r = i % (PT * PT), s1 = r / PT, s0 = r % PT;
       const int64_t gs0 = (int64_t)a0 * W + s0, gs1 = (int64_t)a1 * W + s1;
       if (gs0 >= a.NS0 || gs1 >= a.NS1) continue;
-      a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = Hs[((size_t)h * PTP + s1) * PTP + s0];
+      a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = Hs[(h * PTP + s1) * GP + s0];
     }
   }
 }
@@ -682,7 +721,7 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                      "smem attribute"));
   dim3 grid((unsigned)tiles, (unsigned)ceil_div(s.fs.npt[2], a.lz));
-  asm3_stage12<P, Q, kTile><<<grid, C::NT, smem, st>>>(a, fmap);
+  asm3_stage12<P, Q, kTile><<<grid, C::NT, smem, st>>>(a, fmap);  // C::NT = 512
   IGS_LAUNCH_CHECK("asm3_stage12");
   Asm3bArgs b{};
   b.plan = s.plan;
