@@ -66,6 +66,8 @@ typedef struct {
   const double* points;       /* [num_points] ascending                            */
   int32_t num_elements;       /* K: elements of a per-element rule, else 0         */
   int32_t points_per_element; /* k: points per element of a per-element rule, else 0 */
+  int32_t uniform;            /* 1: equally spaced breakpoints (interior elements share
+                                 one table up to rounding), lets fused kernels hoist it */
 } igs_dir;
 
 /* A trial/test pair on a tensor quadrature plus the coefficient layout:

@@ -41,6 +41,7 @@ class IgsDir(ctypes.Structure):
         ("points", ctypes.c_void_p),
         ("num_elements", ctypes.c_int32),
         ("points_per_element", ctypes.c_int32),
+        ("uniform", ctypes.c_int32),
     ]
 
 

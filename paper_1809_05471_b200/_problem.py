@@ -6,6 +6,8 @@ tensors the struct points at and must live as long as the struct is used.
 
 import ctypes
 
+import numpy as np
+
 from . import _lib
 
 
@@ -36,9 +38,14 @@ def _fill_dir(dst, basis, rule, table, keep):
             and (rule.breakpoints == basis.breakpoints).all()):
         dst.num_elements = rule.elements
         dst.points_per_element = rule.points_per_element
+        bp = basis.breakpoints
+        h = np.diff(bp)
+        dst.uniform = int(basis.max_smoothness and len(h) > 0
+                          and float(np.max(np.abs(h - h[0]))) <= 1e-14 * float(abs(bp[-1] - bp[0])))
     else:
         dst.num_elements = 0
         dst.points_per_element = 0
+        dst.uniform = 0
     del torch
 
 

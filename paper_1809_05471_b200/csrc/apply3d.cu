@@ -30,6 +30,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 namespace igs {
 
 bool fused_shape(const igs_problem* p, const Dims& D, FusedShape* fs) {
@@ -96,6 +98,7 @@ struct ApplyArgs {
   int K0, K1, K2;             // elements (K2 slab-local)
   int z_el_off;               // global element index of local z element 0
   int ntx, nty, nch, ez;      // tiling
+  int uni_x;                  // equally spaced x breakpoints (interior tables shared)
   double* scratch;            // per-item boxes
   int64_t box;                // doubles per box
 };
@@ -127,6 +130,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 // TMA: one 4D box (points of one element, 8 lines, 1 point layer, all planes).
+// L2 prefetch of one TMA box (no shared memory, no barrier): keeps HBM busy
+// while the CTA is in its shared-memory-only phases.
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
   asm volatile(
@@ -139,7 +149,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 // Tile geometry and shared-memory plan.  Q2B point layers of z are processed
 // per batch; warp w owns (point layer w / NLG of the batch, line group
 // w % NLG) in the X phase and sweeps all EX elements of its 8 lines.
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_>
 struct Cfg {
   static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
   static_assert(Q % Q2B == 0, "batches tile the element's point layers");
@@ -157,7 +167,7 @@ struct Cfg {
   static constexpr int NV = STIFF ? 3 : 1;     // (y, z) variants: 00, 10, 01
   static constexpr int NPL = (MASS ? 1 : 0) + (STIFF ? 6 : 0);  // coefficient planes
   static constexpr int QE = (Q + 1) & ~1;      // TMA box width (16-byte multiple)
-  static constexpr int STG = 3;                // TMA stages per warp
+  static constexpr int STG = STG_;             // TMA stages per warp
   static constexpr int FST = NPL * 8 * QE;     // doubles per stage
   static constexpr int LXR = FYP * RP;         // one [n1][n0] plane
   static constexpr int XR = P * LXR;           // x ring (P DoF layers)
@@ -171,12 +181,15 @@ struct Cfg {
   static constexpr int FS = NW * STG * FST;    // coefficient staging
   static constexpr int TOTAL = FS + XR + AQ + CQ + SQ + YR + TBX + TBY + TBZ + WW;
   static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t);
+  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the tile allows
 };
 
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF>
-__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
-    apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap) {
-  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>;
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_>
+__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
+                                  Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::MINB)
+    apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap,
+                   const __grid_constant__ CUtensorMap fmap_row) {
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>;
   constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY;
   constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR, STG = C::STG, FST = C::FST, QE = C::QE;
   constexpr int NLG = C::NLG, NB = C::NB, CQL = C::CQL, NA = C::NA, NV = C::NV;
@@ -210,6 +223,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
   // layer (batch·Q2B + w/NLG) and line group w%NLG, element by element; each
   // (batch, element) is one TMA box, STG boxes in flight per warp.
   const int wq = warp / NLG, wlg = warp % NLG;
+  static_assert(EX % STG == 0 && (EX / STG) % 2 == 0, "ring stage/parity must be static per element");
+  // every element of the tile interior (e in [P-1, K0-P]): one shared table
+  const bool tile_uniform = a.uni_x && ex0 >= P - 1 && ex0 + EX - 1 <= a.K0 - P;
   const int ntask = (z1 - z0) * NB * EX;
   uint64_t* mybar = bars + warp * STG;
   double* mystage = Fs + warp * STG * FST;
@@ -219,6 +235,13 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
     uint64_t* bar = mybar + idx % STG;
     mbar_expect_tx(bar, (unsigned)(FST * sizeof(double)));
     tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + ex) * Q, ey0 * Q + wlg * 8, zq, 0);
+  };
+  // L2 prefetch of this warp's whole 8-line x row of task batch `batch`
+  // (one box of TX points: long contiguous DRAM bursts)
+  auto prefetch_batch = [&](int batch) {
+    if (batch * EX >= ntask) return;
+    const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
+    tma_prefetch_4d(&fmap_row, ex0 * Q, ey0 * Q + wlg * 8, zq, 0);
   };
   if (tid < NW * STG) mbar_init(bars + tid, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -278,8 +301,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
       const int q2 = b * Q2B + qb;
       const double s0 = Sq[(qb * NA + 0) * LXR + o];
       const double s1 = STIFF ? Sq[(qb * NA + 1) * LXR + o] : 0.0;
-      Sq[(qb * NA + 0) * LXR + o] = 0.0;
-      if (STIFF) Sq[(qb * NA + 1) * LXR + o] = 0.0;
 #pragma unroll
       for (int j = 0; j < P; ++j) {
         double v = fma(Tz[(0 * 8 + q2) * 8 + j], s0, *yrow[j]);
@@ -300,6 +321,8 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
     __syncthreads();
 
     for (int b = 0; b < NB; ++b) {
+      // stream the next batch's coefficients into L2 while this one computes
+      if (lane == 0) prefetch_batch((e2 - z0) * NB + b + 1);
       // ---- Z^T(previous batch) + Z(this batch) + clear S ---------------------
       if (b > 0)
         for (int i = tid; i < FY * FX; i += NT) zt_item(e2, b - 1, i);
@@ -360,13 +383,30 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
         double* Crow = Cb + line * RP;  // C (then R) row of this lane's line
         const bool line_ok = (ey0 + line / Q) < a.K1;
         const double wyz = Wz[q2] * Wy[line];
+        const int widx0 = widx;         // = batch·EX: ring stage ex % STG, parity (ex/STG) & 1
         // running X^T window over columns [ex, ex+8): lane m holds ex+2m, ex+2m+1
         double w00[2] = {0.0, 0.0}, w10[2] = {0.0, 0.0}, w01[2] = {0.0, 0.0};
         const int qn = (g >> 1) + 4 * (g & 1);  // D column n -> point q(n)
-#pragma unroll 2
-        for (int ex = 0; ex < EX; ++ex, ++widx) {
+        // table fragments: forward B^T[j][q(n)] and transpose B[q][j], both
+        // levels; hoisted when every element of the tile is interior
+        double fb0[2], fb1[2], tb0[2], tb1[2];
+        auto load_tab = [&](int ex) {
           const double* T0 = Tx + (ex * 2 + 0) * 64;
           const double* T1 = Tx + (ex * 2 + 1) * 64;
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            fb0[s] = T0[qn * 8 + m + 4 * s];
+            fb1[s] = STIFF ? T1[qn * 8 + m + 4 * s] : 0.0;
+            tb0[s] = T0[(m + 4 * s) * 8 + g];
+            tb1[s] = STIFF ? T1[(m + 4 * s) * 8 + g] : 0.0;
+          }
+        };
+        if (tile_uniform) load_tab(0);
+        // point validity masks (the lane's points q = m and m + 4)
+        const double msk0 = (m < Q) ? 1.0 : 0.0, msk1 = (m + 4 < Q) ? 1.0 : 0.0;
+#pragma unroll
+        for (int ex = 0; ex < EX; ++ex) {
+          if (!tile_uniform) load_tab(ex);
           // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  D column n
           // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
           // are points q = m and m + 4: the A-fragment columns of the
@@ -375,56 +415,48 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             const int j = m + 4 * s;
-            const double fb0 = T0[qn * 8 + j];
             const double c0 = Crow[ex + j];
-            if (MASS) dmma(u[0], u[1], c0, fb0);
+            if (MASS) dmma(u[0], u[1], c0, fb0[s]);
             if (STIFF) {
-              const double fb1 = T1[qn * 8 + j];
               const double c1 = Crow[CQL + ex + j];
               const double c2 = Crow[2 * CQL + ex + j];
-              dmma(ux[0], ux[1], c0, fb1);
-              dmma(uy[0], uy[1], c1, fb0);
-              dmma(uz[0], uz[1], c2, fb0);
+              dmma(ux[0], ux[1], c0, fb1[s]);
+              dmma(uy[0], uy[1], c1, fb0[s]);
+              dmma(uz[0], uz[1], c2, fb0[s]);
             }
           }
           // coefficients of (element ex, these 8 lines, point layer q2)
-          mbar_wait(mybar + widx % STG, (unsigned)((widx / STG) & 1));
-          const double* F = mystage + (widx % STG) * FST;
-          const bool ok = (ex0 + ex) < a.K0 && line_ok;
+          mbar_wait(mybar + ex % STG, (unsigned)((ex / STG) & 1));
+          const double* F = mystage + (ex % STG) * FST + g * QE + m;  // [plane][line][q]
+          const double rowm = ((ex0 + ex) < a.K0 && line_ok) ? wyz : 0.0;
           double g0[2], gx[2], gy[2], gz[2];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int q = m + 4 * c;
-            g0[c] = gx[c] = gy[c] = gz[c] = 0.0;
-            if (q < Q && ok) {
-              const double* f = F + g * QE + q;  // [plane][line][q]
-              const double w = wyz * Wx[ex * Q + q];
-              if (MASS) g0[c] = w * (f[pc * 8 * QE] * u[c]);
-              if (STIFF) {
-                const double f00 = f[p00 * 8 * QE], f11 = f[p11 * 8 * QE], f22 = f[p22 * 8 * QE];
-                const double f01 = f[p01 * 8 * QE], f02 = f[p02 * 8 * QE], f12 = f[p12 * 8 * QE];
-                gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
-                gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
-                gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
-              }
+            const double* f = F + 4 * c;
+            const double w = rowm * (c == 0 ? msk0 : msk1) * Wx[(ex * Q + q) < TX ? ex * Q + q : 0];
+            if (MASS) g0[c] = w * (f[pc * 8 * QE] * u[c]);
+            if (STIFF) {
+              const double f00 = f[p00 * 8 * QE], f11 = f[p11 * 8 * QE], f22 = f[p22 * 8 * QE];
+              const double f01 = f[p01 * 8 * QE], f02 = f[p02 * 8 * QE], f12 = f[p12 * 8 * QE];
+              gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
+              gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
+              gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
             }
           }
           __syncwarp();
-          if (lane == 0 && widx + STG < ntask) {
+          if (lane == 0 && widx0 + ex + STG < ntask) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(widx + STG);
+            issue(widx0 + ex + STG);
           }
           // transpose into the window: W^T[line][j] += Σ_q g^T[line][q] · B[q][j]
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
-            const int q = m + 4 * s;
-            const double tb0 = T0[q * 8 + g];
-            if (MASS) dmma(w00[0], w00[1], g0[s], tb0);
+            if (MASS) dmma(w00[0], w00[1], g0[s], tb0[s]);
             if (STIFF) {
-              const double tb1 = T1[q * 8 + g];
-              dmma(w00[0], w00[1], gx[s], tb1);
-              dmma(w10[0], w10[1], gy[s], tb0);
-              dmma(w01[0], w01[1], gz[s], tb0);
+              dmma(w00[0], w00[1], gx[s], tb1[s]);
+              dmma(w10[0], w10[1], gy[s], tb0[s]);
+              dmma(w01[0], w01[1], gz[s], tb0[s]);
             }
           }
           // column ex is complete (no later element touches it): store it over
@@ -451,6 +483,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
             }
           }
         }
+        widx = widx0 + EX;
         // remaining columns [EX, EX + 8): lane m holds EX + 2m + c
         __syncwarp();
 #pragma unroll
@@ -467,13 +500,16 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
       }
       __syncthreads();
 
-      // ---- Y^T (DMMA): S_v[ey+j][n0] += Σ_q By[q][j] · R[ey*Q+q][n0] ----------
+      // ---- Y^T (DMMA): S_v[n1][n0] = Σ_ey Σ_q By[q][n1-ey] · R[ey*Q+q][n0] ------
+      // Sliding 8-row window over n1 (rows = lanes g): after element ey, row
+      // ey is final (lanes g = 0) and the window moves down one row (4 lanes).
       for (int t = warp; t < Q2B * NA * 2; t += NW) {
         const int qb = t / (NA * 2), grp = (t / 2) % NA, nt = t & 1;
         const double* Rb = Cq + qb * NV * CQL;
         double* Sb = Sq + (qb * NA + grp) * LXR;
+        double d[2] = {0.0, 0.0};
+#pragma unroll
         for (int ey = 0; ey < EY; ++ey) {
-          double d[2] = {0.0, 0.0};
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             const int q = m + 4 * s;
@@ -486,10 +522,18 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>::NT, 1)
               dmma(d[0], d[1], t0, Rb[2 * CQL + o]);
             }
           }
-          double* srow = Sb + (ey + g) * RP + nt * 8 + 2 * m;
-          srow[0] += d[0];
-          srow[1] += d[1];
-          __syncwarp();
+          if (g == 0) {
+            Sb[ey * RP + nt * 8 + 2 * m] = d[0];
+            Sb[ey * RP + nt * 8 + 2 * m + 1] = d[1];
+          }
+          d[0] = __shfl_down_sync(0xffffffffu, d[0], 4);
+          d[1] = __shfl_down_sync(0xffffffffu, d[1], 4);
+          if (g == 7) d[0] = d[1] = 0.0;
+        }
+        // rows EY .. FY-1 of the window (lane row g -> n1 = EY + g)
+        if (EY + g < FY) {
+          Sb[(EY + g) * RP + nt * 8 + 2 * m] = d[0];
+          Sb[(EY + g) * RP + nt * 8 + 2 * m + 1] = d[1];
         }
       }
       __syncthreads();
@@ -565,13 +609,23 @@ __global__ void apply_reduce_kernel(const ReduceArgs r) {
 struct Launch {
   int EX, EY, NT, NPL, QE;
   size_t smem;
-  void (*kernel)(ApplyArgs, CUtensorMap);
+  void (*kernel)(ApplyArgs, CUtensorMap, CUtensorMap);
 };
 
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2>
 Launch make_launch() {
-  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF>;
-  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF>};
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG>;
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG>};
+}
+
+// Development switch (IGS_APPLY_VARIANT) for comparing tile shapes on the box.
+int apply_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IGS_APPLY_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 // Tile shapes per order: EY·Q lines in groups of 8, Q2B point layers per
@@ -584,9 +638,17 @@ bool pick(int P, int Q, Launch* L) {
     case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF>(); return true;
     case 4: *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>(); return true;
     case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
-    case 6: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF>(); return true;
+    case 6:
+      if (apply_variant() == 1) *L = make_launch<6, 6, 8, 4, 2, MASS, STIFF, 4>();
+      else if (apply_variant() == 2) *L = make_launch<6, 6, 8, 4, 2, MASS, STIFF, 2>();
+      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
+      return true;
     case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
-    case 8: *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF>(); return true;
+    case 8:
+      if (apply_variant() == 1) *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 2>();
+      else if (apply_variant() == 2) *L = make_launch<8, 8, 8, 2, 2, MASS, STIFF, 2>();
+      else *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 4>();
+      return true;
     default: return false;
   }
 }
@@ -630,7 +692,7 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
 // cuTensorMapEncodeTiled comes from the driver through the runtime's entry
 // point query, so the library does not link libcuda directly.
 igs_status coeff_tensor_map(CUtensorMap* map, const double* planes, int64_t pstride, const Dims& D,
-                            const Launch& L) {
+                            const Launch& L, unsigned box0) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -642,7 +704,7 @@ igs_status coeff_tensor_map(CUtensorMap* map, const double* planes, int64_t pstr
   }
   cuuint64_t dims[4] = {(cuuint64_t)D.x[0], (cuuint64_t)D.x[1], (cuuint64_t)D.x[2], (cuuint64_t)L.NPL};
   cuuint64_t strides[3] = {(cuuint64_t)D.x[0] * 8, (cuuint64_t)(D.x[0] * D.x[1]) * 8, (cuuint64_t)pstride * 8};
-  cuuint32_t boxd[4] = {(cuuint32_t)L.QE, 8u, 1u, (cuuint32_t)L.NPL};
+  cuuint32_t boxd[4] = {(cuuint32_t)box0, 8u, 1u, (cuuint32_t)L.NPL};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(planes), dims, strides,
                       boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -701,15 +763,17 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
   a.X0 = D.x[0]; a.X1 = D.x[1];
   a.K0 = (int)s.nel[0]; a.K1 = (int)s.nel[1]; a.K2 = (int)s.nel[2];
   a.z_el_off = (p->slab_lo || p->slab_hi) ? p->slab_lo : 0;
+  a.uni_x = p->trial[0].uniform;
   a.ntx = t.ntx; a.nty = t.nty; a.nch = t.nch; a.ez = t.ez;
   a.scratch = reinterpret_cast<double*>(ws);
   a.box = t.box;
-  CUtensorMap fmap;
-  IGS_TRY(coeff_tensor_map(&fmap, planes, p->plane_stride, D, L));
+  CUtensorMap fmap, fmap_row;
+  IGS_TRY(coeff_tensor_map(&fmap, planes, p->plane_stride, D, L, (unsigned)L.QE));
+  IGS_TRY(coeff_tensor_map(&fmap_row, planes, p->plane_stride, D, L, (unsigned)(L.EX * L.QE)));
   IGS_TRY(cuda_check(cudaFuncSetAttribute(L.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)L.smem), "smem attribute"));
   unsigned grid = (unsigned)(t.ntx * t.nty * t.nch);
-  L.kernel<<<grid, L.NT, L.smem, st>>>(a, fmap);
+  L.kernel<<<grid, L.NT, L.smem, st>>>(a, fmap, fmap_row);
   IGS_LAUNCH_CHECK("apply3d_kernel");
   if (flags & IGS_FLAG_KERNEL_ONLY) return IGS_OK;
   ReduceArgs r{};
