@@ -1,0 +1,206 @@
+"""GPU tests of SPEC properties and edge cases beyond the golden vectors:
+general spaces on the generic kernels (Petrov-Galerkin, reduced smoothness,
+custom rules, convection), symmetry, measure identities, row-range and
+slab (multi-GPU partition) execution, error behaviour."""
+
+import numpy as np
+import pytest
+
+from oracle import igs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den else 1.0)
+
+
+def _mods():
+    from paper_1809_05471_b200 import (bspline, geometry, matfree, quadrature, sumfac, tensorspace,
+                                       workloads)
+
+    return bspline, quadrature, tensorspace, geometry, sumfac, matfree, workloads
+
+
+def _oracle_space(order, knots, points, weights):
+    return O.Space1D(order, knots, points, weights, max_deriv=1)
+
+
+def _dense_problem(trial_kv, test_kv, rules, F, theta, eta):
+    bspline, quadrature, tensorspace, geometry, sumfac, matfree, workloads = _mods()
+    trial = [bspline.UnivariateBasis(kv) for kv in trial_kv]
+    test = [bspline.UnivariateBasis(kv) for kv in test_kv]
+    quad = quadrature.TensorQuadrature(rules)
+    field = geometry.CoefficientField(theta, eta, F, quad.shape)
+    return sumfac.AssemblyProblem(trial, test, quad, field)
+
+
+def _check_against_kron(prob, F, theta, eta):
+    bspline, quadrature, tensorspace, geometry, sumfac, matfree, workloads = _mods()
+    A = sumfac.assemble(prob)
+    pat = prob.pattern()
+    tr = [_oracle_space(b.order, b.kv.knots, r.points, r.weights) for b, r in zip(prob.trial, prob.quad.rules)]
+    te = [_oracle_space(b.order, b.kv.knots, r.points, r.weights) for b, r in zip(prob.test, prob.quad.rules)]
+    pairs = [O.pattern_1d(t.lo, t.hi, s.lo, s.hi, t.points) for t, s in zip(tr, te)]
+    indptr, indices = O.tensor_csr(pairs, [t.num_basis for t in tr], [s.num_basis for s in te])
+    np.testing.assert_array_equal(pat.indptr, indptr)
+    np.testing.assert_array_equal(pat.indices, indices)
+    Ar = O.assemble_kron(tr, te, theta, eta, F)
+    vals = O.values_on_pattern(Ar, indptr, indices)
+    assert rel(A.values_np(), vals) <= 1e-12
+    return A, Ar
+
+
+def test_petrov_galerkin_reduced_smoothness_and_convection(cuda):
+    """Trial order 3 with double interior knots, test order 2, 2D, full
+    first-order coupling with a non-symmetric F (convection)."""
+    bspline, quadrature, *_ = _mods()
+    tk = [bspline.uniform_open_knots(3, 4, interior_multiplicity=2), bspline.uniform_open_knots(3, 3)]
+    sk = [bspline.uniform_open_knots(2, 4), bspline.uniform_open_knots(2, 3)]
+    rules = [quadrature.per_element_rule(np.unique(k.knots), 3) for k in tk]
+    theta = [(0, 0), (1, 0), (0, 1)]
+    eta = [(0, 0), (1, 0), (0, 1)]
+    npts = rules[0].num_points * rules[1].num_points
+    F = np.random.default_rng(3).uniform(-1, 1, (npts, 3, 3))
+    prob = _dense_problem(tk, sk, rules, F, theta, eta)
+    _check_against_kron(prob, F, theta, eta)
+
+
+def test_custom_rule_and_dir_order(cuda):
+    bspline, quadrature, tensorspace, geometry, sumfac, *_ = _mods()
+    kv = bspline.uniform_open_knots(3, 3)
+    # trapezoid-like custom rule: still assembles, generic path
+    pts = np.linspace(0.02, 0.98, 13)
+    w = np.full(13, 1.0 / 13)
+    rules = [quadrature.custom_rule(pts, w), quadrature.per_element_rule(np.unique(kv.knots), 2)]
+    theta = eta = geometry.first_order_derivative_set(2)
+    npts = 13 * rules[1].num_points
+    F = np.zeros((npts, 3, 3))
+    F[:, 0, 0] = 1.0
+    F[:, 1, 1] = F[:, 2, 2] = 2.0
+    prob = _dense_problem([kv, kv], [kv, kv], rules, F, theta, eta)
+    A, _ = _check_against_kron(prob, F, theta, eta)
+    B = sumfac.assemble(prob, dir_order=(1, 0))
+    assert rel(B.values_np(), A.values_np()) <= 1e-13
+
+
+@pytest.mark.parametrize("d,p,K,kind", [(2, 5, 12, 2), (3, 4, 6, 3), (2, 3, 9, 1), (3, 3, 5, 2)])
+def test_symmetry_and_mass_total(cuda, d, p, K, kind):
+    *_, sumfac, matfree, workloads = _mods()
+    prob = workloads.make_problem(d, p, K, kind, seed=4)
+    A = sumfac.assemble(prob).to_scipy()
+    asym = (A - A.T)
+    assert np.sqrt((asym.data ** 2).sum()) / np.sqrt((A.data ** 2).sum()) <= 1e-12
+    if kind == 1:
+        # c ~ U[0.5, 1.5] mass: 1ᵀ M 1 = ∫ c over the unit cube (quadrature)
+        planes = prob.coeff.planes.cpu().numpy()[0]
+        w = prob.quad.flat_weights()
+        one = np.ones(A.shape[0])
+        assert abs(one @ (A @ one) - np.dot(w, planes)) <= 1e-12
+
+
+def test_assembly_row_ranges_match_full(cuda):
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.sumfac import _run_assembly
+
+    for (d, p, K, kind) in [(3, 4, 5, 3), (2, 5, 9, 2)]:
+        prob = workloads.make_problem(d, p, K, kind, seed=8)
+        full = sumfac.assemble(prob).values_np()
+        pat = prob.pattern()
+        nrows = pat.shape[0]
+        cut = [0, nrows // 3, (2 * nrows) // 3, nrows]
+        parts = []
+        for lo, hi in zip(cut[:-1], cut[1:]):
+            vals = _run_assembly(prob, None, None, None, 0, (lo, hi)).cpu().numpy()
+            a, b = pat.indptr[lo], pat.indptr[hi]
+            parts.append(vals[: b - a])
+        np.testing.assert_array_equal(np.concatenate(parts), full)
+    del torch
+
+
+def test_max_nnz_capacity_error(cuda):
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.errors import CapacityError
+
+    prob = workloads.make_problem(3, 4, 5, 3, max_nnz=1000)
+    with pytest.raises(CapacityError):
+        prob.pattern()
+
+
+def test_apply_1d_and_2d_generic_against_oracle(cuda):
+    *_, sumfac, matfree, workloads = _mods()
+    for (d, p, K, kind) in [(1, 5, 20, 3), (2, 4, 10, 3)]:
+        prob = workloads.make_problem(d, p, K, kind, seed=2)
+        op = matfree.MatrixFreeOperator(prob)
+        assert not op.fused
+        x = O.recipe_x(prob.shape[1], seed=1)
+        y = matfree.apply(op, x)
+        sp = [O.uniform_space(p, K) for _ in range(d)]
+        ths = O.first_order_set(d)
+        y_ref = O.apply(sp, p, ths, ths, O.plane_map(d, kind), prob.coeff.planes.cpu().numpy(), x)
+        assert rel(y, y_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("p,kind,world", [(6, 2, 3), (8, 3, 2), (4, 3, 4)])
+def test_slab_partition_on_one_gpu(cuda, p, kind, world):
+    """The multi-GPU decomposition executed slab by slab on one GPU with the
+    halo exchange replaced by device copies: must equal the full apply."""
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.sharded import SlabPartition
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
+
+    K = 16
+    bases, quad = workloads.spaces(3, p, K)
+    full_planes = workloads.synthetic_planes(3, list(quad.shape), kind, seed=5)
+    full = AssemblyProblem(bases, bases, quad, workloads.field_from_planes(3, kind, full_planes, quad.shape))
+    n = full.shape[1]
+    layer_n = n // (K + p - 1)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)
+    y_full = matfree.MatrixFreeOperator(full).apply_device(x)
+    part = SlabPartition(K, p, world)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    layer_pts = quad.num_points // quad.shape[-1]
+    for r in range(world):
+        lo, hi = part.elements(r)
+        planes = full_planes[:, lo * p * layer_pts: hi * p * layer_pts].contiguous()
+        field = workloads.field_from_planes(3, kind, planes, quad.shape, slab=(lo, hi))
+        prob = AssemblyProblem(bases, bases, quad, field)
+        op = matfree.MatrixFreeOperator(prob)
+        assert op.fused
+        xl = x[lo * layer_n: (hi + p - 1) * layer_n].contiguous()
+        yl = op.apply_device(xl)
+        y[lo * layer_n: (hi + p - 1) * layer_n] += yl   # ghost reduce
+    err = float(torch.linalg.vector_norm(y - y_full) / torch.linalg.vector_norm(y_full))
+    assert err <= 1e-13
+
+
+def test_apply_accumulate_flag_and_determinism(cuda):
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    prob = workloads.make_problem(3, 6, 9, 2, seed=12)
+    op = matfree.MatrixFreeOperator(prob)
+    n = prob.shape[1]
+    x = torch.randn(n, dtype=torch.float64, device="cuda")
+    y1 = op.apply_device(x)
+    y2 = op.apply_device(x)
+    assert torch.equal(y1, y2), "fixed summation order: bit-reproducible"
+    y3 = y1.clone()
+    op.apply_device(x, y3, accumulate=True)
+    assert torch.allclose(y3, 2 * y1, rtol=1e-15, atol=0)
+
+
+def test_eval_field_partition_of_unity(cuda):
+    *_, sumfac, matfree, workloads = _mods()
+    torch = cuda
+    prob = workloads.make_problem(3, 4, 5, 3)
+    n = prob.shape[1]
+    u = matfree.eval_field(prob, torch.ones(n, dtype=torch.float64, device="cuda"), (0, 0, 0))
+    assert float(torch.abs(u - 1).max()) <= 1e-14
+    du = matfree.eval_field(prob, torch.ones(n, dtype=torch.float64, device="cuda"), (1, 0, 0))
+    assert float(torch.abs(du).max()) <= 1e-11
