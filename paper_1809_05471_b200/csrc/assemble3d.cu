@@ -375,7 +375,8 @@ struct Asm3bArgs {
 template <int P, int Q>
 __global__ void __launch_bounds__(128) asm3_stage3(const Asm3bArgs a) {
   constexpr int W = 2 * P - 1;
-  __shared__ double w2s[Q][4][P][P];  // W2^{v}[jn][jm] at the element's Q points
+  // W_z^{v2(h)}[jn][jm] at the element's Q points, h innermost (zero for h >= nh)
+  __shared__ __align__(16) double w2s[Q][P][P][4];
   const AsmPlan& pl = a.plan;
   const int nh = pl.nh;
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -423,28 +424,49 @@ __global__ void __launch_bounds__(128) asm3_stage3(const Asm3bArgs a) {
       const int e2 = eb + r;
       if (e2 >= K2) break;
       __syncthreads();
-      for (int i = threadIdx.x; i < Q * 4 * P * P; i += nthr) {
-        int jm = i % P, jn = (i / P) % P, v = (i / (P * P)) % 4, q = i / (4 * P * P);
-        int64_t x = (int64_t)e2 * Q + q;
-        double w = a.tab.wts[2][x];
-        double bn = (v & 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v & 1) * P + jn) * a.tab.X[2] + x];
-        double bm = (v >> 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v >> 1) * P + jm) * a.tab.X[2] + x];
-        w2s[q][v][jn][jm] = (w * bn) * bm;
+      for (int i = threadIdx.x; i < Q * P * P * 4; i += nthr) {
+        const int hh = i % 4, jn = (i / 4) % P, jm = (i / (4 * P)) % P, q = i / (4 * P * P);
+        double val = 0.0;
+        if (hh < nh) {
+          const int v = pl.h_v2[hh];
+          const int64_t x = (int64_t)e2 * Q + q;
+          const double w = a.tab.wts[2][x];
+          const double bn = (v & 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v & 1) * P + jn) * a.tab.X[2] + x];
+          const double bm = (v >> 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v >> 1) * P + jm) * a.tab.X[2] + x];
+          val = (w * bn) * bm;
+        }
+        w2s[q][jm][jn][hh] = val;
       }
       __syncthreads();
       if (valid) {
+        const double* hp = a.H + (int64_t)e2 * Q * nh * a.NS1 * a.NS0 + s1 * a.NS0 + s0;
+        const int64_t hs = a.NS1 * a.NS0;  // stride between (x2, h) planes
+        double h[4], hn[4];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) h[hh] = hh < nh ? __ldg(hp + hh * hs) : 0.0;
+#pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const int64_t x2 = (int64_t)e2 * Q + q;
-          double h[4];
-          for (int hh = 0; hh < nh; ++hh) h[hh] = __ldg(a.H + ((x2 * nh + hh) * a.NS1 + s1) * a.NS0 + s0);
+          if (q + 1 < Q) {  // software pipeline: next point layer's loads in flight
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) hn[hh] = hh < nh ? __ldg(hp + ((q + 1) * nh + hh) * hs) : 0.0;
+          }
 #pragma unroll
           for (int jm = 0; jm < P; ++jm)
 #pragma unroll
             for (int jn = 0; jn < P; ++jn) {
-              double s = ring[(r + jm) % P][jn - jm + P - 1];
-              for (int hh = 0; hh < nh; ++hh) s = fma(w2s[q][pl.h_v2[hh]][jn][jm], h[hh], s);
-              ring[(r + jm) % P][jn - jm + P - 1] = s;
+              const double2 wa = *reinterpret_cast<const double2*>(&w2s[q][jm][jn][0]);
+              const double2 wb = *reinterpret_cast<const double2*>(&w2s[q][jm][jn][2]);
+              double sacc = ring[(r + jm) % P][jn - jm + P - 1];
+              sacc = fma(wa.x, h[0], sacc);
+              sacc = fma(wa.y, h[1], sacc);
+              sacc = fma(wb.x, h[2], sacc);
+              sacc = fma(wb.y, h[3], sacc);
+              ring[(r + jm) % P][jn - jm + P - 1] = sacc;
             }
+          if (q + 1 < Q) {
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh) h[hh] = hn[hh];
+          }
         }
         // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
         flush(e2, ring[r % P]);
