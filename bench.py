@@ -147,6 +147,51 @@ def cpu_baseline(w, min_seconds=10.0, seed=0):
                       f"numpy oracle apply_slab on {cores} threads, {t:.1f} s"}
 
 
+def assembly_section(reps=5, cpu=True, seed=0):
+    """C3 assembly (d=3, p=4, 64^3, mass+stiffness) measured in the same run:
+    warm assembly (pattern cached, as the reference caches it), CUDA events,
+    nnz/s; roofline against the measured fp64 DMMA peak; CPU baseline = the
+    oracle's independent Kronecker assembly on a reduced mesh (same p)."""
+    import torch
+
+    from paper_1809_05471_b200 import sumfac, workloads
+
+    prob = workloads.make_problem(3, 4, 64, workloads.MASS_STIFF, seed=seed, max_nnz=1 << 40)
+    A = sumfac.assemble(prob)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        A = sumfac.assemble(prob)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nnz = A.nnz
+    npts = prob.quad.num_points
+    b_alg = 8 * prob.coeff.n_planes * npts + 8 * nnz       # planes read + values written
+    flops = 2 * 10_390_000_000                                # merged-block MACs (DESIGN.md §3, K3)
+    p64 = 37.15e12                                            # measured DMMA peak (profiles/r01_fp64_peak.txt)
+    out = {"workload": "C3", "desc": "d3 p4 64^3 mass+stiffness assembly (warm, pattern cached)",
+           "value": nnz / (ms / 1e3), "unit": "nnz/s", "ms": ms, "nnz": nnz, "fused": sumfac.fused_path(prob),
+           "roofline": {"bound": "fp64", "achieved_tflops": flops / (ms / 1e3) / 1e12, "peak_tflops": p64 / 1e12,
+                        "frac": flops / (ms / 1e3) / p64, "hbm_gbs": b_alg / (ms / 1e3) / 1e9,
+                        "alg_bytes": b_alg, "alg_flops": flops}}
+    if cpu:
+        from oracle import igs_oracle as O
+
+        K = 24
+        sp = [O.uniform_space(4, K) for _ in range(3)]
+        planes = O.synthetic_planes(3, [4 * K] * 3, 0, 4 * K, 3, seed)
+        ths = O.first_order_set(3)
+        t0 = time.perf_counter()
+        vals = O.assemble_sumfac(sp, sp, ths, ths, planes, O.plane_map(3, 3))
+        t = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": vals.size / t, "unit": "nnz/s", "cores": 1, "kind": "port",
+                               "sample": f"oracle Alg. 1 restatement (scipy CSR x dense per direction, as the "
+                                         f"reference), p=4, {K}^3 elements, {vals.size} nnz, {t:.2f} s"}
+    return out
+
+
 def run_reference(args, w):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -175,6 +220,7 @@ def main():
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-assembly", action="store_true")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -294,10 +340,17 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e_value = N * args.steps / (e2e_ms / 1e3)
+    fused_flag = op.fused
 
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w)
+    asm = None
+    if rank == 0 and world == 1 and not args.no_assembly:
+        try:
+            asm = assembly_section(cpu=not args.no_cpu_baseline)
+        except Exception as exc:  # the apply line must still print
+            asm = {"error": repr(exc)}
     if rank == 0:
         line = {
             "metric": "matrix-free fp64 apply throughput", "value": value, "unit": "DoF/s",
@@ -315,7 +368,8 @@ def main():
             "gpu_launches": args.steps * (2 if world == 1 else 2),
             "clocks": clk.summary(),
             "cpu_baseline": cb,
-            "fused": op.fused,
+            "fused": fused_flag,
+            "assembly": asm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
