@@ -266,17 +266,46 @@ __global__ void __launch_bounds__(512, 1)
   }
   fill_wtab<P, Q, T>(W0, a.tab, 0, eb0);
   fill_wtab<P, Q, T>(W1, a.tab, 1, eb1);
+  // Per-lane scatter plan: the lane's element-local pairs land in slot
+  // el·W + base; valid for el in [lo, hi) (tile rows and mesh bounds).
+  int base1[NLT][2], lo1[NLT][2], hi1[NLT][2], base2[NLT], lo2[NLT], hi2[NLT];
+#pragma unroll
+  for (int nt = 0; nt < NLT; ++nt) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int pr = nt * 8 + 2 * m4 + c, jn = pr / P, jm = pr % P;
+      base1[nt][c] = (jm - (P - 1)) * W + (jn - jm + P - 1);
+      int lo = P - 1 - jm, hi = P - 1 - jm + T;
+      lo = max(lo, (int)(-eb0) - jn);
+      hi = min(hi, N0 - (int)eb0 - jn);
+      hi = min(hi, N0 - (int)eb0 - jm);
+      lo1[nt][c] = pr < P * P ? lo : 1;
+      hi1[nt][c] = pr < P * P ? hi : 0;
+    }
+    const int pr = nt * 8 + g8, jn = pr / P, jm = pr % P;
+    base2[nt] = (jm - (P - 1)) * W + (jn - jm + P - 1);
+    int lo = P - 1 - jm, hi = P - 1 - jm + T;
+    lo = max(lo, (int)(-eb1) - jn);
+    hi = min(hi, N1 - (int)eb1 - jn);
+    hi = min(hi, N1 - (int)eb1 - jm);
+    lo2[nt] = pr < P * P ? lo : 1;
+    hi2[nt] = pr < P * P ? hi : 0;
+  }
   unsigned phase = 0;
   for (int64_t x2 = z_lo; x2 < z_hi; ++x2, phase ^= 1) {
-    for (int i = tid; i < ng * XRP * GP; i += NT) Gs[i] = 0.0;
+    {
+      double2* G2 = reinterpret_cast<double2*>(Gs);
+      for (int i = tid; i < ng * XRP * GP / 2; i += NT) G2[i] = make_double2(0.0, 0.0);
+    }
     __syncthreads();
     dev::mbar_wait(bar, phase);
     // ---- stage 1: task = (group, y tile); sweep the region's elements -------
     for (int t = warp; t < ng * (XRP / 8); t += NW) {
       const int g = t / (XRP / 8), yt = t % (XRP / 8);
       const int y = yt * 8 + g8;  // A row
-      double* Gg = Gs + g * XRP * GP;
+      double* Gy = Gs + g * XRP * GP + y * GP;
       const int b_lo = pl.g_b0[g], b_hi = b_lo + pl.g_nb[g];
+#pragma unroll
       for (int el = 0; el < ER; ++el) {
         double d[NLT][2];
 #pragma unroll
@@ -295,19 +324,15 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int nt = 0; nt < NLT; ++nt)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int pr = nt * 8 + 2 * m4 + c;
-            if (pr >= P * P) continue;
-            const int jn = pr / P, jm = pr % P;
-            const int m0 = (int)eb0 + el + jm, n0 = (int)eb0 + el + jn;
-            if (m0 < a0 || m0 >= a0 + T || n0 < 0 || n0 >= N0 || m0 >= N0) continue;
-            const int s0 = (m0 - a0) * W + (jn - jm + P - 1);
-            Gg[y * GP + s0] += d[nt][c];
-          }
+          for (int c = 0; c < 2; ++c)
+            if (el >= lo1[nt][c] && el < hi1[nt][c]) Gy[el * W + base1[nt][c]] += d[nt][c];
         __syncwarp();
       }
     }
-    for (int i = tid; i < nh * PTP * GP; i += NT) Hs[i] = 0.0;
+    {
+      double2* H2 = reinterpret_cast<double2*>(Hs);
+      for (int i = tid; i < nh * PTP * GP / 2; i += NT) H2[i] = make_double2(0.0, 0.0);
+    }
     __syncthreads();
     // F is consumed: fetch the next layer's region while stage 2 runs
     if (tid == 0 && x2 + 1 < z_hi) {
@@ -318,8 +343,9 @@ __global__ void __launch_bounds__(512, 1)
     // ---- stage 2: task = (h, s0 tile); sweep the region's y elements ---------
     for (int t = warp; t < nh * (PTP / 8); t += NW) {
       const int h = t / (PTP / 8), st = t % (PTP / 8);
-      double* Hh = Hs + h * PTP * GP;
+      double* Hh = Hs + h * PTP * GP + st * 8 + 2 * m4;
       const int g_lo = pl.h_g0[h], g_hi = g_lo + pl.h_ng[h];
+#pragma unroll
       for (int el = 0; el < ER; ++el) {
         double d[NLT][2];
 #pragma unroll
@@ -336,26 +362,27 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
 #pragma unroll
-        for (int mt = 0; mt < NLT; ++mt) {
-          const int pr = mt * 8 + g8;
-          if (pr >= P * P) continue;
-          const int jn = pr / P, jm = pr % P;
-          const int m1 = (int)eb1 + el + jm, n1 = (int)eb1 + el + jn;
-          if (m1 < a1 || m1 >= a1 + T || n1 < 0 || n1 >= N1 || m1 >= N1) continue;
-          const int s1 = (m1 - a1) * W + (jn - jm + P - 1);
-          Hh[s1 * GP + st * 8 + 2 * m4] += d[mt][0];
-          Hh[s1 * GP + st * 8 + 2 * m4 + 1] += d[mt][1];
-        }
+        for (int mt = 0; mt < NLT; ++mt)
+          if (el >= lo2[mt] && el < hi2[mt]) {
+            double2* dst = reinterpret_cast<double2*>(Hh + (el * W + base2[mt]) * GP);
+            double2 v = *dst;
+            v.x += d[mt][0];
+            v.y += d[mt][1];
+            *dst = v;
+          }
         __syncwarp();
       }
     }
     __syncthreads();
     // ---- write H[x2][h][s1][s0] for the tile's valid slots -------------------
-    for (int i = tid; i < nh * PT * PT; i += NT) {
-      const int h = i / (PT * PT), r = i % (PT * PT), s1 = r / PT, s0 = r % PT;
-      const int64_t gs0 = (int64_t)a0 * W + s0, gs1 = (int64_t)a1 * W + s1;
-      if (gs0 >= a.NS0 || gs1 >= a.NS1) continue;
-      a.H[((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + gs0] = Hs[(h * PTP + s1) * GP + s0];
+    for (int row = warp; row < nh * PT; row += NW) {
+      const int h = row / PT, s1 = row % PT;
+      const int64_t gs1 = (int64_t)a1 * W + s1;
+      if (gs1 >= a.NS1) continue;
+      double* dst = a.H + ((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + (int64_t)a0 * W;
+      const double* src = Hs + (h * PTP + s1) * GP;
+      for (int s0 = lane; s0 < PT; s0 += 32)
+        if ((int64_t)a0 * W + s0 < a.NS0) dst[s0] = src[s0];
     }
   }
 }
