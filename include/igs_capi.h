@@ -181,6 +181,13 @@ igs_status igs_fill_synthetic(int32_t d, const int64_t* point_dims /* host [d] *
                               int64_t z_lo, int64_t z_hi, int32_t kind, uint64_t seed,
                               double* planes, int64_t plane_stride, void* stream);
 
+/* ---- CSR export --------------------------------- */
+/* Writes a HOST CSR matrix as MatrixMarket coordinate `real general`,
+ * 1-based, 17 significant digits. */
+igs_status igs_write_matrix_market(const char* path /* host */, int64_t nrows, int64_t ncols,
+                                   const int64_t* indptr /* host */, const int64_t* indices /* host */,
+                                   const double* values /* host */);
+
 /* ---- K5: halo pack / unpack-add for the slab-partitioned apply ------- */
 /* Copies `nlayers` contiguous DoF layers (layer = N0*N1 doubles) — kept
  * as kernels so they can be captured in CUDA graphs. dst[i] (+)= src[i]. */

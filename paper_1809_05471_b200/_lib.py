@@ -97,6 +97,8 @@ _SIGNATURES = [
       ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]),
     ("igs_layers_copy", ctypes.c_int,
      [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
+    ("igs_write_matrix_market", ctypes.c_int,
+     [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

@@ -23,7 +23,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
           "--expt-relaxed-constexpr"]
 # Per-file extra flags: the tabulation must round like the reference's
 # Python float arithmetic, so no FMA contraction there.
-EXTRA = {"tabulate.cu": ["-fmad=false"]}
+EXTRA = {"tabulate.cu": ["-fmad=false"], "mmio.cpp": ["-Xcompiler", "-fopenmp"]}
 
 SOURCES = [
     "common.cu",
@@ -34,6 +34,7 @@ SOURCES = [
     "synth.cu",
     "apply3d.cu",
     "assemble3d.cu",
+    "mmio.cpp",
 ]
 
 
@@ -57,8 +58,9 @@ def _headers_mtime():
 
 def _compile(name, hdr_mtime, verbose):
     src = os.path.join(CSRC, name)
-    obj = os.path.join(BUILD, name.replace(".cu", ".o"))
-    log = os.path.join(BUILD, name.replace(".cu", ".ptxas.txt"))
+    stem = os.path.splitext(name)[0]
+    obj = os.path.join(BUILD, stem + ".o")
+    log = os.path.join(BUILD, stem + ".ptxas.txt")
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj, False
     cmd = [NVCC, *ARCH, *COMMON, *EXTRA.get(name, []), "-c", src, "-o", obj]
@@ -84,7 +86,7 @@ def build(verbose=False, force=False):
     objs = [r[0] for r in results]
     changed = any(r[1] for r in results)
     if changed or not os.path.exists(LIB_PATH) or force:
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB_PATH, *objs, "-lcudart", "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB_PATH, *objs, "-lcudart", "-lcuda", "-lgomp"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")

@@ -107,6 +107,18 @@ class SparseMatrix:
     def copy(self):
         return SparseMatrix(self.pattern, self.values.clone())
 
+    def write_matrix_market(self, path):
+        """MatrixMarket coordinate export (1-based, 17 significant digits,
+        SPEC.md:426); the CSR arrays are copied to the host once."""
+        lib = _lib.load()
+        indptr = np.ascontiguousarray(self.pattern.indptr, dtype=np.int64)
+        indices = np.ascontiguousarray(self.pattern.indices, dtype=np.int64)
+        values = np.ascontiguousarray(self.values_np(), dtype=np.float64)
+        m, n = self.shape
+        st = lib.igs_write_matrix_market(str(path).encode(), m, n, indptr.ctypes.data, indices.ctypes.data,
+                                         values.ctypes.data)
+        _lib.check(st, "write_matrix_market")
+
 
 def rel_frobenius(a, b):
     """Relative Frobenius distance ||a - b||_F / ||b||_F (sumfac.py:118-141).

@@ -204,3 +204,29 @@ def test_eval_field_partition_of_unity(cuda):
     assert float(torch.abs(u - 1).max()) <= 1e-14
     du = matfree.eval_field(prob, torch.ones(n, dtype=torch.float64, device="cuda"), (1, 0, 0))
     assert float(torch.abs(du).max()) <= 1e-11
+
+
+def test_cg_on_matrix_free_operator_and_matrix_market(cuda, tmp_path):
+    """CG with the fused apply converges to the solution of the assembled
+    system; the assembled matrix round-trips through MatrixMarket."""
+    torch = cuda
+    import scipy.io
+    import scipy.sparse.linalg
+
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.solvers import cg
+
+    prob = workloads.make_problem(3, 4, 6, workloads.MASS_STIFF, seed=3)
+    op = matfree.MatrixFreeOperator(prob)
+    assert op.fused
+    n = prob.shape[1]
+    b = torch.from_numpy(O.recipe_x(n, seed=9)).cuda()
+    x, it, res = cg(lambda v, out: op.apply_device(v, out), b, tol=1e-11, maxiter=2000)
+    assert res <= 1e-11 and it < 2000
+    A = sumfac.assemble(prob)
+    path = tmp_path / "c3_small.mtx"
+    A.write_matrix_market(path)
+    M = scipy.io.mmread(str(path)).tocsr()
+    assert abs(M - A.to_scipy()).max() == 0.0
+    r = M @ x.cpu().numpy() - b.cpu().numpy()
+    assert np.linalg.norm(r) / np.linalg.norm(b.cpu().numpy()) <= 1e-10
