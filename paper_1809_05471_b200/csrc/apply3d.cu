@@ -32,6 +32,22 @@
 
 #include <cstdlib>
 
+#ifdef IGS_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_MARK(k)                                                             \
+  do {                                                                            \
+    if (threadIdx.x == 0) {                                                       \
+      long long now_ = clock64();                                                 \
+      atomicAdd(&g_phase_cycles[k], (unsigned long long)(now_ - phase_t0_));      \
+      phase_t0_ = now_;                                                           \
+    }                                                                             \
+  } while (0)
+#else
+#define PHASE_MARK(k) \
+  do {                \
+  } while (0)
+#endif
+
 namespace igs {
 
 bool fused_shape(const igs_problem* p, const Dims& D, FusedShape* fs) {
@@ -211,6 +227,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, m = lane & 3;  // MMA fragment coordinates
   const int item = blockIdx.x;
+#ifdef IGS_PHASE_TIMING
+  long long phase_t0_ = clock64();
+#endif
   const int tx = item % a.ntx;
   const int ty = (item / a.ntx) % a.nty;
   const int tz = item / (a.ntx * a.nty);
@@ -321,8 +340,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     __syncthreads();
 
     for (int b = 0; b < NB; ++b) {
-      // stream the next batch's coefficients into L2 while this one computes
-      if (lane == 0) prefetch_batch((e2 - z0) * NB + b + 1);
+      PHASE_MARK(0);  // element setup / previous batch tail
       // ---- Z^T(previous batch) + Z(this batch) + clear S ---------------------
       if (b > 0)
         for (int i = tid; i < FY * FX; i += NT) zt_item(e2, b - 1, i);
@@ -342,6 +360,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       }
       __syncthreads();
 
+      PHASE_MARK(1);  // Z (+ Z^T of the previous batch)
       // ---- Y (DMMA): C_vw[q1][n0] = Σ_j By_w[q1][j] · A_v[ey+j][n0] ----------
       for (int t = warp; t < Q2B * EY * 2; t += NW) {
         const int qb = t / (EY * 2), ey = (t / 2) % EY, nt = t & 1;
@@ -375,6 +394,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       }
       __syncthreads();
 
+      PHASE_MARK(2);  // Y
       // ---- X (DMMA) + pointwise + X^T (DMMA), warp-private rows ---------------
       {
         const int q2 = b * Q2B + wq;
@@ -426,7 +446,13 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
             }
           }
           // coefficients of (element ex, these 8 lines, point layer q2)
+#ifdef IGS_PHASE_TIMING
+          long long tw0_ = clock64();
+#endif
           mbar_wait(mybar + ex % STG, (unsigned)((ex / STG) & 1));
+#ifdef IGS_PHASE_TIMING
+          if (tid == 0) atomicAdd(&g_phase_cycles[5], (unsigned long long)(clock64() - tw0_));
+#endif
           const double* F = mystage + (ex % STG) * FST + g * QE + m;  // [plane][line][q]
           const double rowm = ((ex0 + ex) < a.K0 && line_ok) ? wyz : 0.0;
           double g0[2], gx[2], gy[2], gz[2];
@@ -444,11 +470,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
               gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
             }
           }
-          __syncwarp();
-          if (lane == 0 && widx0 + ex + STG < ntask) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(widx0 + ex + STG);
-          }
           // transpose into the window: W^T[line][j] += Σ_q g^T[line][q] · B[q][j]
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
@@ -459,6 +480,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
               dmma(w01[0], w01[1], gz[s], tb0[s]);
             }
           }
+          // every lane's reads of this stage have been consumed (the MMAs above
+          // depend on them): hand the stage to the next box of this warp
+          __syncwarp();
+          if (lane == 0 && widx0 + ex + STG < ntask) issue(widx0 + ex + STG);
           // column ex is complete (no later element touches it): store it over
           // C's column ex, which no later element reads, then slide the window.
           __syncwarp();
@@ -500,6 +525,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       }
       __syncthreads();
 
+      PHASE_MARK(3);  // X
       // ---- Y^T (DMMA): S_v[n1][n0] = Σ_ey Σ_q By[q][n1-ey] · R[ey*Q+q][n0] ------
       // Sliding 8-row window over n1 (rows = lanes g): after element ey, row
       // ey is final (lanes g = 0) and the window moves down one row (4 lanes).
@@ -538,6 +564,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       }
       __syncthreads();
     }
+    PHASE_MARK(4);  // Y^T of the last batch
     // last Z^T of the element, flush DoF layer e2 (complete for this chunk)
     for (int i = tid; i < FY * FX; i += NT) {
       zt_item(e2, NB - 1, i);
@@ -793,3 +820,15 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
 }
 
 }  // namespace igs
+
+#ifdef IGS_PHASE_TIMING
+// Debug-only (built by tools/phase_timing.py): read and reset the per-phase
+// cycle counters of thread 0 of every CTA.
+extern "C" void igs_debug_phase_cycles(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+}
+#endif
