@@ -424,28 +424,28 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         if (tile_uniform) load_tab(0);
         // point validity masks (the lane's points q = m and m + 4)
         const double msk0 = (m < Q) ? 1.0 : 0.0, msk1 = (m + 4 < Q) ? 1.0 : 0.0;
+        // software pipeline: C fragments of element ex+1 are loaded while ex
+        // computes (element ex only ever writes column ex, below them)
+        double cf[3][2], cn[3][2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          cf[0][s] = Crow[m + 4 * s];
+          cf[1][s] = STIFF ? Crow[CQL + m + 4 * s] : 0.0;
+          cf[2][s] = STIFF ? Crow[2 * CQL + m + 4 * s] : 0.0;
+        }
 #pragma unroll
         for (int ex = 0; ex < EX; ++ex) {
           if (!tile_uniform) load_tab(ex);
-          // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  D column n
-          // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
-          // are points q = m and m + 4: the A-fragment columns of the
-          // transposed product below (no shuffles).
-          double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
+          if (ex + 1 < EX) {
 #pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int j = m + 4 * s;
-            const double c0 = Crow[ex + j];
-            if (MASS) dmma(u[0], u[1], c0, fb0[s]);
-            if (STIFF) {
-              const double c1 = Crow[CQL + ex + j];
-              const double c2 = Crow[2 * CQL + ex + j];
-              dmma(ux[0], ux[1], c0, fb1[s]);
-              dmma(uy[0], uy[1], c1, fb0[s]);
-              dmma(uz[0], uz[1], c2, fb0[s]);
+            for (int s = 0; s < 2; ++s) {
+              cn[0][s] = Crow[ex + 1 + m + 4 * s];
+              cn[1][s] = STIFF ? Crow[CQL + ex + 1 + m + 4 * s] : 0.0;
+              cn[2][s] = STIFF ? Crow[2 * CQL + ex + 1 + m + 4 * s] : 0.0;
             }
           }
-          // coefficients of (element ex, these 8 lines, point layer q2)
+          // coefficients of (element ex, these 8 lines, point layer q2): wait
+          // for the TMA box first so its shared-memory reads overlap the MMAs
 #ifdef IGS_PHASE_TIMING
           long long tw0_ = clock64();
 #endif
@@ -454,17 +454,44 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           if (tid == 0) atomicAdd(&g_phase_cycles[5], (unsigned long long)(clock64() - tw0_));
 #endif
           const double* F = mystage + (ex % STG) * FST + g * QE + m;  // [plane][line][q]
+          double fv[7][2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const double* f = F + 4 * c;
+            if (MASS) fv[0][c] = f[pc * 8 * QE];
+            if (STIFF) {
+              fv[1][c] = f[p00 * 8 * QE];
+              fv[2][c] = f[p11 * 8 * QE];
+              fv[3][c] = f[p22 * 8 * QE];
+              fv[4][c] = f[p01 * 8 * QE];
+              fv[5][c] = f[p02 * 8 * QE];
+              fv[6][c] = f[p12 * 8 * QE];
+            }
+          }
+          // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  D column n
+          // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
+          // are points q = m and m + 4: the A-fragment columns of the
+          // transposed product below (no shuffles).
+          double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (MASS) dmma(u[0], u[1], cf[0][s], fb0[s]);
+            if (STIFF) {
+              dmma(ux[0], ux[1], cf[0][s], fb1[s]);
+              dmma(uy[0], uy[1], cf[1][s], fb0[s]);
+              dmma(uz[0], uz[1], cf[2][s], fb0[s]);
+            }
+          }
           const double rowm = ((ex0 + ex) < a.K0 && line_ok) ? wyz : 0.0;
           double g0[2], gx[2], gy[2], gz[2];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int q = m + 4 * c;
-            const double* f = F + 4 * c;
             const double w = rowm * (c == 0 ? msk0 : msk1) * Wx[(ex * Q + q) < TX ? ex * Q + q : 0];
-            if (MASS) g0[c] = w * (f[pc * 8 * QE] * u[c]);
+            if (MASS) g0[c] = w * (fv[0][c] * u[c]);
             if (STIFF) {
-              const double f00 = f[p00 * 8 * QE], f11 = f[p11 * 8 * QE], f22 = f[p22 * 8 * QE];
-              const double f01 = f[p01 * 8 * QE], f02 = f[p02 * 8 * QE], f12 = f[p12 * 8 * QE];
+              const double f00 = fv[1][c], f11 = fv[2][c], f22 = fv[3][c];
+              const double f01 = fv[4][c], f02 = fv[5][c], f12 = fv[6][c];
               gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
               gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
               gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
@@ -507,6 +534,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
               w01[1] = (m == 3) ? 0.0 : nx;
             }
           }
+#pragma unroll
+          for (int v = 0; v < 3; ++v)
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) cf[v][s2] = cn[v][s2];
         }
         widx = widx0 + EX;
         // remaining columns [EX, EX + 8): lane m holds EX + 2m + c
