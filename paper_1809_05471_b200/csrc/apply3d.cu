@@ -192,8 +192,8 @@ struct Cfg {
   static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
   static constexpr int SQ = Q2B * NA * LXR;    // S per point layer of the batch
   static constexpr int YR = P * LXR;           // y ring
-  static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 128;  // [e][v][q8][j8]
-  static constexpr int WW = TX + TY + 8;
+  static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 256;  // [e][v][q8][j8]; Tz double-buffered
+  static constexpr int WW = TX + TY + 16;
   static constexpr int FS = NW * STG * FST;    // coefficient staging
   static constexpr int TOTAL = FS + XR + AQ + CQ + SQ + YR + TBX + TBY + TBZ + WW;
   static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t);
@@ -218,11 +218,11 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   double* Yr = Sq + C::SQ;      // [P][FYP][RP]
   double* Tx = Yr + C::YR;      // [EX][2][8][8]
   double* Ty = Tx + C::TBX;     // [EY][2][8][8]
-  double* Tz = Ty + C::TBY;     // [2][8][8]
-  double* Wx = Tz + C::TBZ;     // [TX]
+  double* Tzb = Ty + C::TBY;    // [2 buffers][2][8][8]
+  double* Wx = Tzb + C::TBZ;    // [TX]
   double* Wy = Wx + TX;         // [TY]
-  double* Wz = Wy + TY;         // [8]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Wz + 8);  // [NW][STG]
+  double* Wzb = Wy + TY;        // [2 buffers][8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Wzb + 16);  // [NW][STG]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, m = lane & 3;  // MMA fragment coordinates
@@ -262,8 +262,12 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
     tma_prefetch_4d(&fmap_row, ex0 * Q, ey0 * Q + wlg * 8, zq, 0);
   };
+  // lanes past the box width of odd Q read neighbouring stage memory (masked
+  // by zero weights): keep it finite
+  for (int i = tid; i < C::FS; i += NT) Fs[i] = 0.0;
   if (tid < NW * STG) mbar_init(bars + tid, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // zeros before TMA writes
   __syncthreads();
   if (lane == 0)
     for (int i = 0; i < STG && i < ntask; ++i) issue(i);
@@ -291,17 +295,33 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     int64_t gg = (int64_t)ey0 * Q + i;
     if (gg < a.X1) Wy[i] = a.wts[1][gg];
   }
+  // asynchronous 8-byte copies (LDGSTS) with zero fill past the domain: the
+  // next element's x layer and z tables stream in behind the last batch
+  auto cp8 = [](double* dst, const double* src, bool ok) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0)
+                 : "memory");
+  };
   auto load_layer = [&](int n2) {
     double* dst = Xr + (n2 % P) * LXR;
     for (int i = tid; i < FY * FX; i += NT) {
       int n0 = i % FX, n1 = i / FX;
       int64_t g0 = (int64_t)ex0 + n0, g1 = (int64_t)ey0 + n1;
-      double v = 0.0;
-      if (g0 < a.N0 && g1 < a.N1 && n2 < a.N2) v = __ldg(a.x + ((int64_t)n2 * a.N1 + g1) * a.N0 + g0);
-      dst[n1 * RP + n0] = v;
+      const bool ok = g0 < a.N0 && g1 < a.N1 && n2 < a.N2;
+      cp8(dst + n1 * RP + n0, ok ? a.x + ((int64_t)n2 * a.N1 + g1) * a.N0 + g0 : a.x, ok);
     }
   };
+  auto load_ztab = [&](int e2, int zb) {
+    const int gz = e2 + a.z_el_off;
+    for (int i = tid; i < 2 * Q * P; i += NT) {
+      int j = i % P, q = (i / P) % Q, v = i / (P * Q);
+      cp8(Tzb + zb * 128 + (v * 8 + q) * 8 + j, a.vals[2] + ((int64_t)v * P + j) * a.xtab[2] + (int64_t)gz * Q + q,
+          true);
+    }
+    for (int i = tid; i < Q; i += NT) cp8(Wzb + zb * 8 + i, a.wts[2] + (int64_t)gz * Q + i, true);
+  };
   for (int l = 0; l < P; ++l) load_layer(z0 + l);
+  if (z0 < z1) load_ztab(z0, 0);
 
   // plane slots inside a TMA stage
   const int pc = a.pl_c;
@@ -310,7 +330,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 
   // Z^T of the Q2B point layers of batch `b` into the y ring (item mapping
   // (n1, n0) identical in every phase that touches the ring).
-  auto zt_item = [&](int e2, int b, int i) {
+  auto zt_item = [&](const double* Tz, int e2, int b, int i) {
     const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
     double* yrow[P];
 #pragma unroll
@@ -331,19 +351,17 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 
   int widx = 0;  // this warp's running TMA task index
   for (int e2 = z0; e2 < z1; ++e2) {
-    const int gz = e2 + a.z_el_off;
-    for (int i = tid; i < 2 * Q * P; i += NT) {
-      int j = i % P, q = (i / P) % Q, v = i / (P * Q);
-      Tz[(v * 8 + q) * 8 + j] = a.vals[2][((int64_t)v * P + j) * a.xtab[2] + (int64_t)gz * Q + q];
-    }
-    for (int i = tid; i < Q; i += NT) Wz[i] = a.wts[2][(int64_t)gz * Q + i];
+    const int zb = (e2 - z0) & 1;
+    const double* Tz = Tzb + zb * 128;
+    const double* Wz = Wzb + zb * 8;
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     for (int b = 0; b < NB; ++b) {
       PHASE_MARK(0);  // element setup / previous batch tail
       // ---- Z^T(previous batch) + Z(this batch) + clear S ---------------------
       if (b > 0)
-        for (int i = tid; i < FY * FX; i += NT) zt_item(e2, b - 1, i);
+        for (int i = tid; i < FY * FX; i += NT) zt_item(Tz, e2, b - 1, i);
       for (int i = tid; i < Q2B * FY * FX; i += NT) {
         const int qb = i / (FY * FX), r = i % (FY * FX);
         const int n0 = r % FX, n1 = r / FX, o = n1 * RP + n0;
@@ -359,6 +377,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         if (STIFF) Aq[(qb * NA + 1) * LXR + o] = a1;
       }
       __syncthreads();
+      if (b == NB - 1) {  // x slot e2 % P and the other z-table buffer are free now
+        load_layer(e2 + P);
+        if (e2 + 1 < z1) load_ztab(e2 + 1, zb ^ 1);
+      }
 
       PHASE_MARK(1);  // Z (+ Z^T of the previous batch)
       // ---- Y (DMMA): C_vw[q1][n0] = Σ_j By_w[q1][j] · A_v[ey+j][n0] ----------
@@ -406,24 +428,25 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         const int widx0 = widx;         // = batch·EX: ring stage ex % STG, parity (ex/STG) & 1
         // running X^T window over columns [ex, ex+8): lane m holds ex+2m, ex+2m+1
         double w00[2] = {0.0, 0.0}, w10[2] = {0.0, 0.0}, w01[2] = {0.0, 0.0};
-        const int qn = (g >> 1) + 4 * (g & 1);  // D column n -> point q(n)
-        // table fragments: forward B^T[j][q(n)] and transpose B[q][j], both
-        // levels; hoisted when every element of the tile is interior
+        // table fragments: forward B^T[j][q = n] (D column n is point n, so a
+        // lane's two D values are the adjacent points 2m, 2m+1) and the
+        // transpose B[q][j] with the k-chunk s covering points q = 2m + s;
+        // hoisted when every element of the tile is interior
         double fb0[2], fb1[2], tb0[2], tb1[2];
         auto load_tab = [&](int ex) {
           const double* T0 = Tx + (ex * 2 + 0) * 64;
           const double* T1 = Tx + (ex * 2 + 1) * 64;
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
-            fb0[s] = T0[qn * 8 + m + 4 * s];
-            fb1[s] = STIFF ? T1[qn * 8 + m + 4 * s] : 0.0;
-            tb0[s] = T0[(m + 4 * s) * 8 + g];
-            tb1[s] = STIFF ? T1[(m + 4 * s) * 8 + g] : 0.0;
+            fb0[s] = T0[g * 8 + m + 4 * s];
+            fb1[s] = STIFF ? T1[g * 8 + m + 4 * s] : 0.0;
+            tb0[s] = T0[(2 * m + s) * 8 + g];
+            tb1[s] = STIFF ? T1[(2 * m + s) * 8 + g] : 0.0;
           }
         };
         if (tile_uniform) load_tab(0);
-        // point validity masks (the lane's points q = m and m + 4)
-        const double msk0 = (m < Q) ? 1.0 : 0.0, msk1 = (m + 4 < Q) ? 1.0 : 0.0;
+        // point validity masks (the lane's points q = 2m and 2m + 1)
+        const double msk0 = (2 * m < Q) ? 1.0 : 0.0, msk1 = (2 * m + 1 < Q) ? 1.0 : 0.0;
         // software pipeline: C fragments of element ex+1 are loaded while ex
         // computes (element ex only ever writes column ex, below them)
         double cf[3][2], cn[3][2];
@@ -453,25 +476,26 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 #ifdef IGS_PHASE_TIMING
           if (tid == 0) atomicAdd(&g_phase_cycles[5], (unsigned long long)(clock64() - tw0_));
 #endif
-          const double* F = mystage + (ex % STG) * FST + g * QE + m;  // [plane][line][q]
+          // [plane][line][q]: the lane's points 2m, 2m+1 as one 16-byte load
+          const double* F = mystage + (ex % STG) * FST + g * QE + 2 * m;
           double fv[7][2];
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const double* f = F + 4 * c;
-            if (MASS) fv[0][c] = f[pc * 8 * QE];
-            if (STIFF) {
-              fv[1][c] = f[p00 * 8 * QE];
-              fv[2][c] = f[p11 * 8 * QE];
-              fv[3][c] = f[p22 * 8 * QE];
-              fv[4][c] = f[p01 * 8 * QE];
-              fv[5][c] = f[p02 * 8 * QE];
-              fv[6][c] = f[p12 * 8 * QE];
-            }
+          auto ld2 = [&](int pl, double* o) {
+            const double2 v = *reinterpret_cast<const double2*>(F + pl * 8 * QE);
+            o[0] = v.x;
+            o[1] = v.y;
+          };
+          if (MASS) ld2(pc, fv[0]);
+          if (STIFF) {
+            ld2(p00, fv[1]);
+            ld2(p11, fv[2]);
+            ld2(p22, fv[3]);
+            ld2(p01, fv[4]);
+            ld2(p02, fv[5]);
+            ld2(p12, fv[6]);
           }
-          // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  D column n
-          // holds point q(n) = (n >> 1) + 4 (n & 1), so a lane's two D values
-          // are points q = m and m + 4: the A-fragment columns of the
-          // transposed product below (no shuffles).
+          // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  A lane's two
+          // D values (points 2m, 2m+1) are its A-fragment columns of the two
+          // k-chunks of the transposed product below (no shuffles).
           double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
@@ -486,7 +510,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           double g0[2], gx[2], gy[2], gz[2];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int q = m + 4 * c;
+            const int q = 2 * m + c;
             const double w = rowm * (c == 0 ? msk0 : msk1) * Wx[(ex * Q + q) < TX ? ex * Q + q : 0];
             if (MASS) g0[c] = w * (fv[0][c] * u[c]);
             if (STIFF) {
@@ -598,15 +622,14 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     PHASE_MARK(4);  // Y^T of the last batch
     // last Z^T of the element, flush DoF layer e2 (complete for this chunk)
     for (int i = tid; i < FY * FX; i += NT) {
-      zt_item(e2, NB - 1, i);
+      zt_item(Tz, e2, NB - 1, i);
       const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
       double* yr = Yr + (e2 % P) * LXR + o;
       box[(int64_t)(e2 - z0) * FY * FX + i] = *yr;
       *yr = 0.0;
     }
-    load_layer(e2 + P);
-    __syncthreads();
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   // trailing P-1 DoF layers [z1, z1 + P - 1)
   for (int l = z1; l < z1 + P - 1; ++l) {
     const double* yr = Yr + (l % P) * LXR;
