@@ -190,7 +190,8 @@ struct Cfg {
   static constexpr int AQ = Q2B * NA * LXR;    // A per point layer of the batch
   static constexpr int CQL = TYP * RP;         // one C/R variant plane
   static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
-  static constexpr int SQ = Q2B * NA * LXR;    // S per point layer of the batch
+  static constexpr int NSP = STIFF ? 3 : 1;    // S parts: By0·R00, By1·R10, By0·R01
+  static constexpr int SQ = Q2B * NSP * LXR;   // S per point layer of the batch
   static constexpr int YR = P * LXR;           // y ring
   static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 256;  // [e][v][q8][j8]; Tz double-buffered
   static constexpr int WW = TX + TY + 16;
@@ -338,8 +339,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 #pragma unroll
     for (int qb = 0; qb < Q2B; ++qb) {
       const int q2 = b * Q2B + qb;
-      const double s0 = Sq[(qb * NA + 0) * LXR + o];
-      const double s1 = STIFF ? Sq[(qb * NA + 1) * LXR + o] : 0.0;
+      const double* sp = Sq + qb * C::NSP * LXR + o;
+      const double s0 = STIFF ? sp[0] + sp[LXR] : sp[0];
+      const double s1 = STIFF ? sp[2 * LXR] : 0.0;
 #pragma unroll
       for (int j = 0; j < P; ++j) {
         double v = fma(Tz[(0 * 8 + q2) * 8 + j], s0, *yrow[j]);
@@ -582,12 +584,15 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 
       PHASE_MARK(3);  // X
       // ---- Y^T (DMMA): S_v[n1][n0] = Σ_ey Σ_q By[q][n1-ey] · R[ey*Q+q][n0] ------
+      // One task per (point layer, part, 8-column half): part 0 = By0·R00,
+      // 1 = By1·R10 (both summed into S_0 by Z^T), 2 = By0·R01 (S_1).
       // Sliding 8-row window over n1 (rows = lanes g): after element ey, row
       // ey is final (lanes g = 0) and the window moves down one row (4 lanes).
-      for (int t = warp; t < Q2B * NA * 2; t += NW) {
-        const int qb = t / (NA * 2), grp = (t / 2) % NA, nt = t & 1;
-        const double* Rb = Cq + qb * NV * CQL;
-        double* Sb = Sq + (qb * NA + grp) * LXR;
+      for (int t = warp; t < Q2B * C::NSP * 2; t += NW) {
+        const int qb = t / (C::NSP * 2), part = (t / 2) % C::NSP, nt = t & 1;
+        const double* Rb = Cq + qb * NV * CQL + part * CQL;
+        const double* Tb = Ty + (part == 1 ? 64 : 0);
+        double* Sb = Sq + (qb * C::NSP + part) * LXR;
         double d[2] = {0.0, 0.0};
 #pragma unroll
         for (int ey = 0; ey < EY; ++ey) {
@@ -595,13 +600,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           for (int s = 0; s < 2; ++s) {
             const int q = m + 4 * s;
             const int o = (ey * Q + q) * RP + nt * 8 + g;  // rows < TYP (padding zero)
-            const double t0 = Ty[((ey * 2 + 0) * 8 + q) * 8 + g];
-            if (grp == 0) {
-              dmma(d[0], d[1], t0, Rb[o]);
-              if (STIFF) dmma(d[0], d[1], Ty[((ey * 2 + 1) * 8 + q) * 8 + g], Rb[CQL + o]);
-            } else {
-              dmma(d[0], d[1], t0, Rb[2 * CQL + o]);
-            }
+            dmma(d[0], d[1], Tb[(ey * 16 + q) * 8 + g], Rb[o]);
           }
           if (g == 0) {
             Sb[ey * RP + nt * 8 + 2 * m] = d[0];
@@ -726,9 +725,9 @@ bool pick(int P, int Q, Launch* L) {
       return true;
     case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
     case 8:
-      if (apply_variant() == 1) *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 2>();
+      if (apply_variant() == 1) *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 4>();
       else if (apply_variant() == 2) *L = make_launch<8, 8, 8, 2, 2, MASS, STIFF, 2>();
-      else *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 4>();
+      else *L = make_launch<8, 8, 8, 6, 2, MASS, STIFF, 2>();
       return true;
     default: return false;
   }
