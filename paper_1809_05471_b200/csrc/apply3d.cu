@@ -115,6 +115,7 @@ struct ApplyArgs {
   int z_el_off;               // global element index of local z element 0
   int ntx, nty, nch, ez;      // tiling
   int uni_x;                  // equally spaced x breakpoints (interior tables shared)
+  int l2pf;                   // development: -1 = re-read one box (L2-resident, no HBM stream)
   double* scratch;            // per-item boxes
   int64_t box;                // doubles per box
 };
@@ -179,6 +180,13 @@ struct Cfg {
   static constexpr int NLG = TY / 8;           // line groups
   static constexpr int NW = Q2B * NLG, NT = 32 * NW;
   static constexpr int NB = Q / Q2B;           // batches per element layer
+  // the DoF rows a line group touches in y fit one 8-row MMA operand
+  static constexpr bool y_rows_fit() {
+    for (int lg = 0; lg < NLG; ++lg)
+      if ((lg * 8 + 7) / Q - (lg * 8) / Q + P - 1 > 7) return false;
+    return true;
+  }
+  static_assert(y_rows_fit(), "line group spans more than 8 DoF rows");
   static constexpr int NA = STIFF ? 2 : 1;     // z variants: value, z-derivative
   static constexpr int NV = STIFF ? 3 : 1;     // (y, z) variants: 00, 10, 01
   static constexpr int NPL = (MASS ? 1 : 0) + (STIFF ? 6 : 0);  // coefficient planes
@@ -254,7 +262,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
     uint64_t* bar = mybar + idx % STG;
     mbar_expect_tx(bar, (unsigned)(FST * sizeof(double)));
-    tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + ex) * Q, ey0 * Q + wlg * 8, zq, 0);
+    if (a.l2pf < 0)
+      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, ex0 * Q, ey0 * Q + wlg * 8, 0, 0);
+    else
+      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + ex) * Q, ey0 * Q + wlg * 8, zq, 0);
   };
   // L2 prefetch of this warp's whole 8-line x row of task batch `batch`
   // (one box of TX points: long contiguous DRAM bursts)
@@ -303,6 +314,22 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0)
                  : "memory");
   };
+  // Y fragments of this warp's 8 lines (line = wlg·8 + g lies in element
+  // line / Q at point line % Q): A[g][k] = By_v[line % Q][ynb + k - line / Q]
+  // over DoF rows ynb + k, k = m + 4s (zero outside the element's support)
+  const int ynb = (wlg * 8) / Q;
+  double byA[2][2];
+  __syncthreads();
+  {
+    const int line = wlg * 8 + g, eyl = line / Q, q1 = line % Q;
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int jj = ynb + m + 4 * s - eyl;
+        byA[v][s] = (jj >= 0 && jj < P && (v == 0 || STIFF)) ? Ty[((eyl * 2 + v) * 8 + q1) * 8 + jj] : 0.0;
+      }
+  }
   auto load_layer = [&](int n2) {
     double* dst = Xr + (n2 % P) * LXR;
     for (int i = tid; i < FY * FX; i += NT) {
@@ -385,46 +412,43 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       }
 
       PHASE_MARK(1);  // Z (+ Z^T of the previous batch)
-      // ---- Y (DMMA): C_vw[q1][n0] = Σ_j By_w[q1][j] · A_v[ey+j][n0] ----------
-      for (int t = warp; t < Q2B * EY * 2; t += NW) {
-        const int qb = t / (EY * 2), ey = (t / 2) % EY, nt = t & 1;
-        const double* A0 = Aq + (qb * NA + 0) * LXR;
-        double c00[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0};
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const int j = m + 4 * s;
-          const double t0 = Ty[((ey * 2 + 0) * 8 + g) * 8 + j];
-          const double b0 = A0[(ey + j) * RP + nt * 8 + g];
-          dmma(c00[0], c00[1], t0, b0);
-          if (STIFF) {
-            const double t1 = Ty[((ey * 2 + 1) * 8 + g) * 8 + j];
-            const double b1 = A0[LXR + (ey + j) * RP + nt * 8 + g];
-            dmma(c10[0], c10[1], t1, b0);
-            dmma(c01[0], c01[1], t0, b1);
-          }
-        }
-        if (g < Q) {
-          double* Cb = Cq + qb * NV * CQL;
-          const int o = (ey * Q + g) * RP + nt * 8 + 2 * m;
-          Cb[o] = c00[0];
-          Cb[o + 1] = c00[1];
-          if (STIFF) {
-            Cb[CQL + o] = c10[0];
-            Cb[CQL + o + 1] = c10[1];
-            Cb[2 * CQL + o] = c01[0];
-            Cb[2 * CQL + o + 1] = c01[1];
-          }
-        }
-      }
-      __syncthreads();
-
-      PHASE_MARK(2);  // Y
-      // ---- X (DMMA) + pointwise + X^T (DMMA), warp-private rows ---------------
+      // ---- Y (DMMA), X (DMMA) + pointwise + X^T (DMMA): warp-private rows -----
       {
         const int q2 = b * Q2B + wq;
         const int line = wlg * 8 + g;   // A-fragment / D row
         double* Cb = Cq + wq * NV * CQL;
         double* Crow = Cb + line * RP;  // C (then R) row of this lane's line
+        // Y for this warp's 8 lines: C_vw[line][n0] = Σ_k By_w[line][k] ·
+        // A_v[nb + k][n0] with the banded per-warp fragments byA (k = m + 4s)
+        {
+          const double* A0 = Aq + (wq * NA) * LXR + ynb * RP;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            double c00[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const int o = (m + 4 * s) * RP + nt * 8 + g;
+              const double b0 = A0[o];
+              dmma(c00[0], c00[1], byA[0][s], b0);
+              if (STIFF) {
+                const double b1 = A0[LXR + o];
+                dmma(c10[0], c10[1], byA[1][s], b0);
+                dmma(c01[0], c01[1], byA[0][s], b1);
+              }
+            }
+            double* co = Crow + nt * 8 + 2 * m;
+            co[0] = c00[0];
+            co[1] = c00[1];
+            if (STIFF) {
+              co[CQL] = c10[0];
+              co[CQL + 1] = c10[1];
+              co[2 * CQL] = c01[0];
+              co[2 * CQL + 1] = c01[1];
+            }
+          }
+          __syncwarp();
+        }
+        PHASE_MARK(2);  // Y
         const bool line_ok = (ey0 + line / Q) < a.K1;
         const double wyz = Wz[q2] * Wy[line];
         const int widx0 = widx;         // = batch·EX: ring stage ex % STG, parity (ex/STG) & 1
@@ -843,6 +867,10 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
   a.X0 = D.x[0]; a.X1 = D.x[1];
   a.K0 = (int)s.nel[0]; a.K1 = (int)s.nel[1]; a.K2 = (int)s.nel[2];
   a.z_el_off = (p->slab_lo || p->slab_hi) ? p->slab_lo : 0;
+  {
+    const char* e = getenv("IGS_APPLY_L2PF");
+    a.l2pf = e ? atoi(e) : 0;
+  }
   a.uni_x = p->trial[0].uniform;
   a.ntx = t.ntx; a.nty = t.nty; a.nch = t.nch; a.ez = t.ez;
   a.scratch = reinterpret_cast<double*>(ws);
