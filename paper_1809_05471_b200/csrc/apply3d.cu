@@ -171,12 +171,12 @@ struct Cfg {
   static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
   static_assert(Q % Q2B == 0, "batches tile the element's point layers");
   static constexpr int FX = EX + P - 1, FY = EY + P - 1;
+  static_assert(FY <= 16, "S-row line-group table holds 16 rows");
   static_assert(EX + 7 <= 16, "x footprint must fit two 8-column MMA tiles");
   static constexpr int RP = 20;                // row pitch (16 used columns, bank-spread)
   static constexpr int FYP = EY + 8;           // rows incl. MMA padding
   static constexpr int TX = EX * Q, TY = EY * Q;
   static_assert(TY % 8 == 0, "lines come in MMA groups of 8");
-  static constexpr int TYP = TY + 8;           // lines incl. padding read by Y^T
   static constexpr int NLG = TY / 8;           // line groups
   static constexpr int NW = Q2B * NLG, NT = 32 * NW;
   static constexpr int NB = Q / Q2B;           // batches per element layer
@@ -196,16 +196,18 @@ struct Cfg {
   static constexpr int LXR = FYP * RP;         // one [n1][n0] plane
   static constexpr int XR = P * LXR;           // x ring (P DoF layers)
   static constexpr int AQ = Q2B * NA * LXR;    // A per point layer of the batch
-  static constexpr int CQL = TYP * RP;         // one C/R variant plane
+  static constexpr int CQL = TY * RP;          // one C/R variant plane
   static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
-  static constexpr int NSP = STIFF ? 3 : 1;    // S parts: By0·R00, By1·R10, By0·R01
-  static constexpr int SQ = Q2B * NSP * LXR;   // S per point layer of the batch
+  // Y^T partial sums of one warp: [NA][8 DoF rows][16 columns], the two
+  // 8-column halves swapped on odd rows (conflict-free 16-byte stores)
+  static constexpr int SPW = NA * 8 * 16;
+  static constexpr int SQ = NW * SPW;
   static constexpr int YR = P * LXR;           // y ring
   static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 256;  // [e][v][q8][j8]; Tz double-buffered
   static constexpr int WW = TX + TY + 16;
   static constexpr int FS = NW * STG * FST;    // coefficient staging
   static constexpr int TOTAL = FS + XR + AQ + CQ + SQ + YR + TBX + TBY + TBZ + WW;
-  static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t);
+  static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t) + 16 * sizeof(int);
   static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the tile allows
 };
 
@@ -222,8 +224,8 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   double* Fs = sm;              // [NW][STG][NPL][8][QE]  (TMA destination)
   double* Xr = Fs + C::FS;      // [P][FYP][RP]
   double* Aq = Xr + C::XR;      // [Q2B][NA][FYP][RP]
-  double* Cq = Aq + C::AQ;      // [Q2B][NV][TYP][RP]   (R overwrites C in place)
-  double* Sq = Cq + C::CQ;      // [Q2B][NA][FYP][RP]
+  double* Cq = Aq + C::AQ;      // [Q2B][NV][TY][RP]   (R overwrites C in place)
+  double* Sq = Cq + C::CQ;      // [NW][NA][8][16]     (Y^T partials per warp)
   double* Yr = Sq + C::SQ;      // [P][FYP][RP]
   double* Tx = Yr + C::YR;      // [EX][2][8][8]
   double* Ty = Tx + C::TBX;     // [EY][2][8][8]
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   double* Wy = Wx + TX;         // [TY]
   double* Wzb = Wy + TY;        // [2 buffers][8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(Wzb + 16);  // [NW][STG]
+  int* zr = reinterpret_cast<int*>(bars + NW * STG);       // [FY] line-group range per S row
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, m = lane & 3;  // MMA fragment coordinates
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // line / Q at point line % Q): A[g][k] = By_v[line % Q][ynb + k - line / Q]
   // over DoF rows ynb + k, k = m + 4s (zero outside the element's support)
   const int ynb = (wlg * 8) / Q;
-  double byA[2][2];
+  double byA[2][2], byT[2][2];
   __syncthreads();
   {
     const int line = wlg * 8 + g, eyl = line / Q, q1 = line % Q;
@@ -328,7 +331,21 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       for (int s = 0; s < 2; ++s) {
         const int jj = ynb + m + 4 * s - eyl;
         byA[v][s] = (jj >= 0 && jj < P && (v == 0 || STIFF)) ? Ty[((eyl * 2 + v) * 8 + q1) * 8 + jj] : 0.0;
+        // transpose: A[k = g][line' = m + 4s] = By_v[line' % Q][ynb + g - line' / Q]
+        const int lt = wlg * 8 + m + 4 * s, eyt = lt / Q, qt = lt % Q, jt = ynb + g - eyt;
+        byT[v][s] = (jt >= 0 && jt < P && (v == 0 || STIFF)) ? Ty[((eyt * 2 + v) * 8 + qt) * 8 + jt] : 0.0;
       }
+  }
+  for (int n1 = tid; n1 < FY; n1 += NT) {
+    int lo = NLG, hi = -1;
+    for (int lg = 0; lg < NLG; ++lg) {
+      const int nb = (lg * 8) / Q, ne = (lg * 8 + 7) / Q + P - 1;
+      if (nb <= n1 && n1 <= ne) {
+        lo = min(lo, lg);
+        hi = max(hi, lg);
+      }
+    }
+    zr[n1] = lo | (hi << 8);
   }
   auto load_layer = [&](int n2) {
     double* dst = Xr + (n2 % P) * LXR;
@@ -357,24 +374,35 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   const int p01 = a.pl_a[0][1], p02 = a.pl_a[0][2], p12 = a.pl_a[1][2];
 
   // Z^T of the Q2B point layers of batch `b` into the y ring (item mapping
-  // (n1, n0) identical in every phase that touches the ring).
+  // (n1, n0) identical in every phase that touches the ring).  S row n1 is
+  // the fixed-order sum of the partials of line groups zr[n1] = lo | hi << 8.
   auto zt_item = [&](const double* Tz, int e2, int b, int i) {
     const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
-    double* yrow[P];
-#pragma unroll
-    for (int j = 0; j < P; ++j) yrow[j] = Yr + ((e2 + j) % P) * LXR + o;
+    const int lr = zr[n1], lo = lr & 255, hi = lr >> 8;
+    double s0[Q2B], s1[Q2B];
 #pragma unroll
     for (int qb = 0; qb < Q2B; ++qb) {
-      const int q2 = b * Q2B + qb;
-      const double* sp = Sq + qb * C::NSP * LXR + o;
-      const double s0 = STIFF ? sp[0] + sp[LXR] : sp[0];
-      const double s1 = STIFF ? sp[2 * LXR] : 0.0;
-#pragma unroll
-      for (int j = 0; j < P; ++j) {
-        double v = fma(Tz[(0 * 8 + q2) * 8 + j], s0, *yrow[j]);
-        if (STIFF) v = fma(Tz[(1 * 8 + q2) * 8 + j], s1, v);
-        *yrow[j] = v;
+      double a0 = 0.0, a1 = 0.0;
+      for (int lg = lo; lg <= hi; ++lg) {
+        const int r = n1 - (lg * 8) / Q;
+        const double* sp = Sq + (qb * NLG + lg) * C::SPW + r * 16 + (n0 ^ ((r & 1) << 3));
+        a0 += sp[0];
+        if (STIFF) a1 += sp[128];
       }
+      s0[qb] = a0;
+      s1[qb] = a1;
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      double* yr = Yr + ((e2 + j) % P) * LXR + o;
+      double v = *yr;
+#pragma unroll
+      for (int qb = 0; qb < Q2B; ++qb) {
+        const int q2 = b * Q2B + qb;
+        v = fma(Tz[(0 * 8 + q2) * 8 + j], s0[qb], v);
+        if (STIFF) v = fma(Tz[(1 * 8 + q2) * 8 + j], s1[qb], v);
+      }
+      *yr = v;
     }
   };
 
@@ -603,44 +631,37 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
             }
           }
         }
+        __syncwarp();
+        // Y^T partials of this warp's 8 lines: S_0 = By0·R00 + By1·R10 and
+        // S_1 = By0·R01 over DoF rows ynb + k (fragments byT, k = g)
+        {
+          const double* R0 = Cb + (wlg * 8) * RP;
+          double* Sw = Sq + warp * C::SPW;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const int o = (m + 4 * s) * RP + nt * 8 + g;
+              dmma(d0[0], d0[1], byT[0][s], R0[o]);
+              if (STIFF) {
+                dmma(d0[0], d0[1], byT[1][s], R0[CQL + o]);
+                dmma(d1[0], d1[1], byT[0][s], R0[2 * CQL + o]);
+              }
+            }
+            double* so = Sw + g * 16 + ((nt ^ (g & 1)) << 3) + 2 * m;
+            so[0] = d0[0];
+            so[1] = d0[1];
+            if (STIFF) {
+              so[128] = d1[0];
+              so[129] = d1[1];
+            }
+          }
+        }
       }
       __syncthreads();
 
-      PHASE_MARK(3);  // X
-      // ---- Y^T (DMMA): S_v[n1][n0] = Σ_ey Σ_q By[q][n1-ey] · R[ey*Q+q][n0] ------
-      // One task per (point layer, part, 8-column half): part 0 = By0·R00,
-      // 1 = By1·R10 (both summed into S_0 by Z^T), 2 = By0·R01 (S_1).
-      // Sliding 8-row window over n1 (rows = lanes g): after element ey, row
-      // ey is final (lanes g = 0) and the window moves down one row (4 lanes).
-      for (int t = warp; t < Q2B * C::NSP * 2; t += NW) {
-        const int qb = t / (C::NSP * 2), part = (t / 2) % C::NSP, nt = t & 1;
-        const double* Rb = Cq + qb * NV * CQL + part * CQL;
-        const double* Tb = Ty + (part == 1 ? 64 : 0);
-        double* Sb = Sq + (qb * C::NSP + part) * LXR;
-        double d[2] = {0.0, 0.0};
-#pragma unroll
-        for (int ey = 0; ey < EY; ++ey) {
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int q = m + 4 * s;
-            const int o = (ey * Q + q) * RP + nt * 8 + g;  // rows < TYP (padding zero)
-            dmma(d[0], d[1], Tb[(ey * 16 + q) * 8 + g], Rb[o]);
-          }
-          if (g == 0) {
-            Sb[ey * RP + nt * 8 + 2 * m] = d[0];
-            Sb[ey * RP + nt * 8 + 2 * m + 1] = d[1];
-          }
-          d[0] = __shfl_down_sync(0xffffffffu, d[0], 4);
-          d[1] = __shfl_down_sync(0xffffffffu, d[1], 4);
-          if (g == 7) d[0] = d[1] = 0.0;
-        }
-        // rows EY .. FY-1 of the window (lane row g -> n1 = EY + g)
-        if (EY + g < FY) {
-          Sb[(EY + g) * RP + nt * 8 + 2 * m] = d[0];
-          Sb[(EY + g) * RP + nt * 8 + 2 * m + 1] = d[1];
-        }
-      }
-      __syncthreads();
+      PHASE_MARK(3);  // X (+ Y^T partials)
     }
     PHASE_MARK(4);  // Y^T of the last batch
     // last Z^T of the element, flush DoF layer e2 (complete for this chunk)
