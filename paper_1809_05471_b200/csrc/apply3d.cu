@@ -198,15 +198,11 @@ struct Cfg {
   static constexpr int AQ = Q2B * NA * LXR;    // A per point layer of the batch
   static constexpr int CQL = TY * RP;          // one C/R variant plane
   static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
-  // Y^T partial sums of one warp: [NA][8 DoF rows][16 columns], the two
-  // 8-column halves swapped on odd rows (conflict-free 16-byte stores)
-  static constexpr int SPW = NA * 8 * 16;
-  static constexpr int SQ = NW * SPW;
   static constexpr int YR = P * LXR;           // y ring
   static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 256;  // [e][v][q8][j8]; Tz double-buffered
   static constexpr int WW = TX + TY + 16;
   static constexpr int FS = NW * STG * FST;    // coefficient staging
-  static constexpr int TOTAL = FS + XR + AQ + CQ + SQ + YR + TBX + TBY + TBZ + WW;
+  static constexpr int TOTAL = FS + XR + AQ + CQ + YR + TBX + TBY + TBZ + WW;
   static constexpr size_t SMEM = (size_t)TOTAL * sizeof(double) + NW * STG * sizeof(uint64_t) + 16 * sizeof(int);
   static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the tile allows
 };
@@ -224,9 +220,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   double* Fs = sm;              // [NW][STG][NPL][8][QE]  (TMA destination)
   double* Xr = Fs + C::FS;      // [P][FYP][RP]
   double* Aq = Xr + C::XR;      // [Q2B][NA][FYP][RP]
-  double* Cq = Aq + C::AQ;      // [Q2B][NV][TY][RP]   (R overwrites C in place)
-  double* Sq = Cq + C::CQ;      // [NW][NA][8][16]     (Y^T partials per warp)
-  double* Yr = Sq + C::SQ;      // [P][FYP][RP]
+  // C, then R in place, then the warp's Y^T partials S_v over its own rows
+  double* Cq = Aq + C::AQ;      // [Q2B][NV][TY][RP]
+  double* Yr = Cq + C::CQ;      // [P][FYP][RP]
   double* Tx = Yr + C::YR;      // [EX][2][8][8]
   double* Ty = Tx + C::TBX;     // [EY][2][8][8]
   double* Tzb = Ty + C::TBY;    // [2 buffers][2][8][8]
@@ -254,7 +250,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // layer (batch·Q2B + w/NLG) and line group w%NLG, element by element; each
   // (batch, element) is one TMA box, STG boxes in flight per warp.
   const int wq = warp / NLG, wlg = warp % NLG;
-  static_assert(EX % STG == 0 && (EX / STG) % 2 == 0, "ring stage/parity must be static per element");
+  // ring stage / parity of a task: static per element when STG divides EX
+  // into an even number of rounds, otherwise from the running task index
+  constexpr bool kStaticRing = EX % STG == 0 && (EX / STG) % 2 == 0;
   // every element of the tile interior (e in [P-1, K0-P]): one shared table
   const bool tile_uniform = a.uni_x && ex0 >= P - 1 && ex0 + EX - 1 <= a.K0 - P;
   const int ntask = (z1 - z0) * NB * EX;
@@ -384,10 +382,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     for (int qb = 0; qb < Q2B; ++qb) {
       double a0 = 0.0, a1 = 0.0;
       for (int lg = lo; lg <= hi; ++lg) {
-        const int r = n1 - (lg * 8) / Q;
-        const double* sp = Sq + (qb * NLG + lg) * C::SPW + r * 16 + (n0 ^ ((r & 1) << 3));
+        const double* sp = Cq + qb * NV * CQL + (lg * 8 + n1 - (lg * 8) / Q) * RP + n0;
         a0 += sp[0];
-        if (STIFF) a1 += sp[128];
+        if (STIFF) a1 += sp[CQL];
       }
       s0[qb] = a0;
       s1[qb] = a1;
@@ -479,7 +476,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         PHASE_MARK(2);  // Y
         const bool line_ok = (ey0 + line / Q) < a.K1;
         const double wyz = Wz[q2] * Wy[line];
-        const int widx0 = widx;         // = batch·EX: ring stage ex % STG, parity (ex/STG) & 1
+        const int widx0 = widx;         // = batch·EX
         // running X^T window over columns [ex, ex+8): lane m holds ex+2m, ex+2m+1
         double w00[2] = {0.0, 0.0}, w10[2] = {0.0, 0.0}, w01[2] = {0.0, 0.0};
         // table fragments: forward B^T[j][q = n] (D column n is point n, so a
@@ -526,12 +523,14 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 #ifdef IGS_PHASE_TIMING
           long long tw0_ = clock64();
 #endif
-          mbar_wait(mybar + ex % STG, (unsigned)((ex / STG) & 1));
+          const int gi = kStaticRing ? ex : widx0 + ex;
+          const int stage = gi % STG;
+          mbar_wait(mybar + stage, (unsigned)((gi / STG) & 1));
 #ifdef IGS_PHASE_TIMING
           if (tid == 0) atomicAdd(&g_phase_cycles[5], (unsigned long long)(clock64() - tw0_));
 #endif
           // [plane][line][q]: the lane's points 2m, 2m+1 as one 16-byte load
-          const double* F = mystage + (ex % STG) * FST + g * QE + 2 * m;
+          const double* F = mystage + stage * FST + g * QE + 2 * m;
           double fv[7][2];
           auto ld2 = [&](int pl, double* o) {
             const double2 v = *reinterpret_cast<const double2*>(F + pl * 8 * QE);
@@ -633,28 +632,31 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         }
         __syncwarp();
         // Y^T partials of this warp's 8 lines: S_0 = By0·R00 + By1·R10 and
-        // S_1 = By0·R01 over DoF rows ynb + k (fragments byT, k = g)
+        // S_1 = By0·R01 over DoF rows ynb + k (fragments byT, k = g), stored
+        // over the warp's own R rows (planes 0 and 1) once all are consumed
         {
           const double* R0 = Cb + (wlg * 8) * RP;
-          double* Sw = Sq + warp * C::SPW;
+          double d0[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, d1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};
+          for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
               const int o = (m + 4 * s) * RP + nt * 8 + g;
-              dmma(d0[0], d0[1], byT[0][s], R0[o]);
+              dmma(d0[nt][0], d0[nt][1], byT[0][s], R0[o]);
               if (STIFF) {
-                dmma(d0[0], d0[1], byT[1][s], R0[CQL + o]);
-                dmma(d1[0], d1[1], byT[0][s], R0[2 * CQL + o]);
+                dmma(d0[nt][0], d0[nt][1], byT[1][s], R0[CQL + o]);
+                dmma(d1[nt][0], d1[nt][1], byT[0][s], R0[2 * CQL + o]);
               }
             }
-            double* so = Sw + g * 16 + ((nt ^ (g & 1)) << 3) + 2 * m;
-            so[0] = d0[0];
-            so[1] = d0[1];
+          __syncwarp();
+          double* so = Cb + (wlg * 8 + g) * RP + 2 * m;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            so[nt * 8] = d0[nt][0];
+            so[nt * 8 + 1] = d0[nt][1];
             if (STIFF) {
-              so[128] = d1[0];
-              so[129] = d1[1];
+              so[CQL + nt * 8] = d1[nt][0];
+              so[CQL + nt * 8 + 1] = d1[nt][1];
             }
           }
         }
@@ -764,9 +766,8 @@ bool pick(int P, int Q, Launch* L) {
     case 4: *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>(); return true;
     case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
     case 6:
-      if (apply_variant() == 1) *L = make_launch<6, 6, 8, 4, 2, MASS, STIFF, 4>();
-      else if (apply_variant() == 2) *L = make_launch<6, 6, 8, 4, 2, MASS, STIFF, 2>();
-      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
+      if (apply_variant() == 1) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
+      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
       return true;
     case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
     case 8:

@@ -28,7 +28,7 @@ from paper_1809_05471_b200 import matfree, workloads  # noqa: E402
 L = _lib.load()
 fn = L.igs_debug_phase_cycles
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-names = ["Y^T+elem-end", "Z", "Y", "X", "last Y^T"]
+names = ["elem-end+barrier", "Z+Z^T", "Y", "X+Y^T", "-"]
 for name in sys.argv[1:] or ["C4", "C5"]:
     c = workloads.CONFIGS[name]
     prob = workloads.make_problem(c["d"], c["p"], c["K"], c["kind"])
