@@ -177,161 +177,139 @@ struct A3Cfg {
   static constexpr int PT = T * W;           // slots per tile per direction
   static constexpr int PTP = (PT + 7) & ~7;  // padded to MMA tiles
   static constexpr int ER = T + P - 1;       // elements in the support region
-  static constexpr int XR = ER * Q;          // points in the region
-  static constexpr int XRP = (XR + 7) & ~7;  // padded to MMA tiles
-  static constexpr int NLP = P * P;          // element-local (n, m) pairs
-  static constexpr int NLT = (NLP + 7) / 8;  // ... in MMA tiles of 8
-  static constexpr int KS = (Q + 3) / 4;     // MMA k-steps per element (points)
-  static constexpr int QP = KS * 4;          // points per element, padded
+  static constexpr int XR = ER * Q;          // points in the region (TMA box width)
+  static constexpr int XRP = (XR + 7) & ~7;  // ... padded to MMA tiles (y rows)
+  static constexpr int XK = (XR + 3) & ~3;   // ... padded to k-steps (x)
   static constexpr int NT = 512, NW = 16;
-  // Row pitches ≡ 8 (mod 16) doubles: the MMA fragment loads that walk 4
-  // rows x 8 consecutive doubles then hit every bank exactly twice.
-  static constexpr int WP = ((NLT * 8 + 7) / 16) * 16 + 8;  // W-table row (pairs)
-  static constexpr int GP = ((PTP + 7) / 16) * 16 + 8;      // G / H row (slots)
-  // shared memory (doubles)
-  static constexpr int WT = ER * 4 * QP * WP;  // W tables [e][v][q][pair] per direction
-  static constexpr size_t smem(int npl, int ng, int nh) {
-    size_t f = ((size_t)npl * XRP * XR + 15) & ~size_t(15);  // coefficient tile [plane][y][x]
-    size_t h = (size_t)nh * PTP * GP;                  // H tile [h][s1][s0]
-    size_t g = (size_t)ng * XRP * GP;                  // G [g][y][s0]
-    return (f + h + g + 2 * (size_t)WT) * sizeof(double) + 16;
+  // Row pitches ≡ 4 (mod 16) doubles: a fragment load that walks 4 rows x 8
+  // consecutive doubles (or 8 rows x 4) then hits every bank once per half-warp.
+  static constexpr int pitch4(int n) { return ((n + 11) / 16) * 16 + 4; }
+  static constexpr int SP = pitch4(PTP);     // rows over slots: W0 tables, G
+  static constexpr int YP = pitch4(XRP);     // rows over y points: W1 tables (transposed)
+  static constexpr int W0T = 4 * XK * SP;    // W0[v][x][s0]
+  static constexpr int W1T = 4 * PTP * YP;   // W1[v][s1][y]
+  // + 4 doubles of zero tail: the last row's k-step padding (x in [XR, XK))
+  static constexpr size_t fdoubles(int npl) { return ((size_t)npl * XRP * XR + 4 + 15) & ~size_t(15); }
+  static constexpr size_t smem(int npl, int ng) {
+    return (fdoubles(npl) + (size_t)ng * XRP * SP + W0T + W1T) * sizeof(double) + 16;
   }
 };
 
-// W^{v}[q][pair] of element e: w(q)·B^θ_{jn}(q)·B^η_{jm}(q), pair = jn·P + jm,
-// v = θ + 2η; zero for padded points/pairs and elements outside the mesh.
-template <int P, int Q, int T>
-__device__ void fill_wtab(double* Wt, const TabArgs& t, int dir, int64_t e_first) {
+// Dense band tables of one direction over the tile's region:
+//   W[v][x][s] = w(x)·B^θ_{n}(x)·B^η_{m}(x)  for slot s = (m - a)·W + (n - m + P - 1),
+// v = θ + 2η; zero where x is outside the mesh/region or (m, n) outside the
+// support of x's element (same product order as _Core.w_matrix).
+// transposed = true stores [v][s][x] (row pitch YP) for the stage-2 A operand.
+template <int P, int Q, int T, bool TRANSPOSED>
+__device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row, int64_t x_first) {
   using C = A3Cfg<P, Q, T>;
-  for (int i = threadIdx.x; i < C::WT; i += C::NT) {
-    const int pr = i % C::WP, q = (i / C::WP) % C::QP, v = (i / (C::WP * C::QP)) % 4,
-              el = i / (C::WP * C::QP * 4);
-    const int64_t e = e_first + el;
+  constexpr int W = C::W;
+  constexpr int NX = TRANSPOSED ? C::XRP : C::XK;
+  constexpr int NS = TRANSPOSED ? C::PTP : C::SP;
+  constexpr int PITCH = TRANSPOSED ? C::YP : C::SP;
+  constexpr int ROWS = TRANSPOSED ? C::PTP : C::XK;
+  constexpr int TOT = 4 * ROWS * PITCH;
+  const int64_t Nf = t.N[dir];
+  for (int i = threadIdx.x; i < TOT; i += C::NT) {
+    const int col = i % PITCH, row = (i / PITCH) % ROWS, v = i / (PITCH * ROWS);
+    const int xl = TRANSPOSED ? col : row, sl = TRANSPOSED ? row : col;
     double val = 0.0;
-    if (pr < C::NLP && q < Q && e >= 0 && e < t.K[dir]) {
-      const int jn = pr / P, jm = pr % P, th = v & 1, et = v >> 1;
-      const int64_t x = e * Q + q;
-      if (th <= t.md[dir] && et <= t.md[dir]) {
-        const double w = t.wts[dir][x];
-        const double bn = t.vals[dir][((int64_t)th * P + jn) * t.X[dir] + x];
-        const double bm = t.vals[dir][((int64_t)et * P + jm) * t.X[dir] + x];
-        val = (w * bn) * bm;
+    if (xl < C::XR && xl < NX && sl < C::PT && sl < NS) {
+      const int64_t x = x_first + xl;
+      const int64_t m = a_row + sl / W, n = m + sl % W - (P - 1);
+      if (x >= 0 && x < t.X[dir] && m < Nf && n >= 0 && n < Nf) {
+        const int64_t e = x / Q;
+        const int64_t jn = n - e, jm = m - e;
+        const int th = v & 1, et = v >> 1;
+        if (jn >= 0 && jn < P && jm >= 0 && jm < P && th <= t.md[dir] && et <= t.md[dir]) {
+          const double w = t.wts[dir][x];
+          const double bn = t.vals[dir][((int64_t)th * P + jn) * t.X[dir] + x];
+          const double bm = t.vals[dir][((int64_t)et * P + jm) * t.X[dir] + x];
+          val = (w * bn) * bm;
+        }
       }
     }
     Wt[i] = val;
   }
 }
 
-// Per (tile of T x T rows, chunk of z point layers), for every layer:
-//   stage 1 (x):  G_g[y][s0] = Σ_{b∈g} Σ_q F_b[y][e0·Q+q] · W0^{v0(b)}_{e0}[q][pair]   (DMMA, M=y N=pair K=q)
-//   stage 2 (y):  H_h[s1][s0] = Σ_{g∈h} Σ_q W1^{v1(g)}_{e1}[pair1][q] · G_g[e1·Q+q][s0] (DMMA, M=pair1 N=s0 K=q)
-// with the element-local pair results overlap-added into band slots by the
-// warp that owns those columns (no races, fixed order).  The coefficient
-// region of the next layer is fetched by TMA while stage 2 runs.
+// k-steps (of 4 points) of the region that touch the tile rows behind slot
+// tile `st`: row r (tile-relative) is supported by region elements [r, r+P-1].
+template <int P, int Q, int T>
+__device__ __forceinline__ void slot_tile_ksteps(int st, int kmax, int& k_lo, int& k_hi) {
+  constexpr int W = 2 * P - 1;
+  const int r_lo = (st * 8) / W;
+  const int r_hi = min(T - 1, (st * 8 + 7) / W);
+  k_lo = (r_lo * Q) / 4;
+  k_hi = min(kmax, ((r_hi + P) * Q + 3) / 4);
+}
+
+// Per (tile of T x T rows, chunk of z point layers), for every layer, as
+// dense banded GEMMs (DMMA m8n8k4, accumulators in registers, no scatter):
+//   stage 1 (x):  G_g[y][s0] = Σ_{b∈g} Σ_x F_b[y][x] · W0^{v0(b)}[x][s0]       (M=y  N=s0 K=x)
+//   stage 2 (y):  H_h[s1][s0] = Σ_{g∈h} Σ_y W1^{v1(g)}[s1][y] · G_g[y][s0]     (M=s1 N=s0 K=y)
+// Each warp task owns one output tile for all groups (balanced); k-steps
+// that cannot touch the task's rows are skipped.  H goes straight from the
+// MMA fragments to HBM; the next layer's coefficient region is fetched by TMA
+// while stage 2 runs.
 template <int P, int Q, int T>
 __global__ void __launch_bounds__(512, 1)
     asm3_stage12(const Asm3Args a, const __grid_constant__ CUtensorMap fmap) {
   using C = A3Cfg<P, Q, T>;
-  constexpr int W = C::W, PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, ER = C::ER;
-  constexpr int NLT = C::NLT, KS = C::KS, QP = C::QP, NT = C::NT, NW = C::NW;
-  constexpr int WP = C::WP, GP = C::GP;
+  constexpr int PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, XK = C::XK;
+  constexpr int NT = C::NT, NW = C::NW, SP = C::SP, YP = C::YP, W = C::W;
   extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
-  const int nb = pl.nb, ng = pl.ng, nh = pl.nh;
-  const size_t fsz = (size_t)a.nplanes * XRP * XR;
-  double* Fs = sm;                                  // [n_planes][XRP y][XR x]   (TMA box)
-  double* Hs = Fs + ((fsz + 15) & ~size_t(15));     // [nh][PTP s1][GP]
-  double* Gs = Hs + (size_t)nh * PTP * GP;          // [ng][XRP y][GP]
-  double* W0 = Gs + (size_t)ng * XRP * GP;          // [ER][4][QP][WP]
-  double* W1 = W0 + C::WT;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(W1 + C::WT);
+  const int ng = pl.ng, nh = pl.nh;
+  const size_t fsz = C::fdoubles(a.nplanes);
+  double* Fs = sm;                   // [n_planes][XRP y][XR x]   (TMA box)
+  double* Gs = Fs + fsz;             // [ng][XRP y][SP]
+  double* W0 = Gs + (size_t)ng * XRP * SP;  // [4][XK x][SP]
+  double* W1 = W0 + C::W0T;                  // [4][PTP s1][YP]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(W1 + C::W1T);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, m4 = lane & 3;
-  const int N0 = (int)a.tab.N[0], N1 = (int)a.tab.N[1];
   const int t0 = blockIdx.x % a.nt0, t1 = blockIdx.x / a.nt0;
   const int64_t z_lo = (int64_t)blockIdx.y * a.lz;
   const int64_t z_hi = min64(a.tab.X[2], z_lo + a.lz);
   const int a0 = t0 * T, a1 = t1 * T;                     // first rows of the tile
-  const int64_t eb0 = a0 - (P - 1), eb1 = a1 - (P - 1);   // first region elements
-  const int xb0 = (int)eb0 * Q, xb1 = (int)eb1 * Q;       // first region points (may be < 0)
-  const unsigned fbytes = (unsigned)(fsz * sizeof(double));
+  const int xb0 = (a0 - (P - 1)) * Q, xb1 = (a1 - (P - 1)) * Q;  // first region points (may be < 0)
+  const unsigned fbytes = (unsigned)((size_t)a.nplanes * XRP * XR * sizeof(double));
+  for (size_t i = (size_t)a.nplanes * XRP * XR + tid; i < fsz; i += NT) Fs[i] = 0.0;  // k-step tail
   if (tid == 0) {
     dev::mbar_init(bar, 1);
     dev::fence_mbar_init();
   }
+  dev::fence_proxy_async();
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && z_lo < z_hi) {
     dev::mbar_expect_tx(bar, fbytes);
     dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)z_lo, 0);
   }
-  fill_wtab<P, Q, T>(W0, a.tab, 0, eb0);
-  fill_wtab<P, Q, T>(W1, a.tab, 1, eb1);
-  // Per-lane scatter plan: the lane's element-local pairs land in slot
-  // el·W + base; valid for el in [lo, hi) (tile rows and mesh bounds).
-  int base1[NLT][2], lo1[NLT][2], hi1[NLT][2], base2[NLT], lo2[NLT], hi2[NLT];
-#pragma unroll
-  for (int nt = 0; nt < NLT; ++nt) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int pr = nt * 8 + 2 * m4 + c, jn = pr / P, jm = pr % P;
-      base1[nt][c] = (jm - (P - 1)) * W + (jn - jm + P - 1);
-      int lo = P - 1 - jm, hi = P - 1 - jm + T;
-      lo = max(lo, (int)(-eb0) - jn);
-      hi = min(hi, N0 - (int)eb0 - jn);
-      hi = min(hi, N0 - (int)eb0 - jm);
-      lo1[nt][c] = pr < P * P ? lo : 1;
-      hi1[nt][c] = pr < P * P ? hi : 0;
-    }
-    const int pr = nt * 8 + g8, jn = pr / P, jm = pr % P;
-    base2[nt] = (jm - (P - 1)) * W + (jn - jm + P - 1);
-    int lo = P - 1 - jm, hi = P - 1 - jm + T;
-    lo = max(lo, (int)(-eb1) - jn);
-    hi = min(hi, N1 - (int)eb1 - jn);
-    hi = min(hi, N1 - (int)eb1 - jm);
-    lo2[nt] = pr < P * P ? lo : 1;
-    hi2[nt] = pr < P * P ? hi : 0;
-  }
+  fill_band_table<P, Q, T, false>(W0, a.tab, 0, a0, xb0);
+  fill_band_table<P, Q, T, true>(W1, a.tab, 1, a1, xb1);
+  __syncthreads();
   unsigned phase = 0;
   for (int64_t x2 = z_lo; x2 < z_hi; ++x2, phase ^= 1) {
-    {
-      double2* G2 = reinterpret_cast<double2*>(Gs);
-      for (int i = tid; i < ng * XRP * GP / 2; i += NT) G2[i] = make_double2(0.0, 0.0);
-    }
-    __syncthreads();
     dev::mbar_wait(bar, phase);
-    // ---- stage 1: task = (group, y tile); sweep the region's elements -------
-    for (int t = warp; t < ng * (XRP / 8); t += NW) {
-      const int g = t / (XRP / 8), yt = t % (XRP / 8);
-      const int y = yt * 8 + g8;  // A row
-      double* Gy = Gs + g * XRP * GP + y * GP;
-      const int b_lo = pl.g_b0[g], b_hi = b_lo + pl.g_nb[g];
-#pragma unroll
-      for (int el = 0; el < ER; ++el) {
-        double d[NLT][2];
-#pragma unroll
-        for (int nt = 0; nt < NLT; ++nt) d[nt][0] = d[nt][1] = 0.0;
+    // ---- stage 1: task = (y tile, s0 tile), all groups --------------------------
+    for (int t = warp; t < (XRP / 8) * (PTP / 8); t += NW) {
+      const int yt = t / (PTP / 8), st = t % (PTP / 8);
+      int k_lo, k_hi;
+      slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
+      const int y = yt * 8 + g8;
+      for (int g = 0; g < ng; ++g) {
+        double d0 = 0.0, d1 = 0.0;
+        const int b_lo = pl.g_b0[g], b_hi = b_lo + pl.g_nb[g];
         for (int b = b_lo; b < b_hi; ++b) {
-          const double* Fb = Fs + pl.b_plane[b] * (XRP * XR) + y * XR + el * Q;
-          const double* Wb = W0 + (el * 4 + pl.b_v0[b]) * (QP * WP);
-#pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            const int q = ks * 4 + m4;
-            const double av = q < Q ? Fb[q] : 0.0;
-#pragma unroll
-            for (int nt = 0; nt < NLT; ++nt) dmma_a(d[nt][0], d[nt][1], av, Wb[q * WP + nt * 8 + g8]);
-          }
+          const double* Fb = Fs + pl.b_plane[b] * (XRP * XR) + y * XR + m4;
+          const double* Wb = W0 + pl.b_v0[b] * (XK * SP) + m4 * SP + st * 8 + g8;
+          for (int ks = k_lo; ks < k_hi; ++ks) dmma_a(d0, d1, Fb[ks * 4], Wb[ks * 4 * SP]);
         }
-#pragma unroll
-        for (int nt = 0; nt < NLT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-            if (el >= lo1[nt][c] && el < hi1[nt][c]) Gy[el * W + base1[nt][c]] += d[nt][c];
-        __syncwarp();
+        double* Gd = Gs + (g * XRP + y) * SP + st * 8 + 2 * m4;
+        Gd[0] = d0;
+        Gd[1] = d1;
       }
-    }
-    {
-      double2* H2 = reinterpret_cast<double2*>(Hs);
-      for (int i = tid; i < nh * PTP * GP / 2; i += NT) H2[i] = make_double2(0.0, 0.0);
     }
     __syncthreads();
     // F is consumed: fetch the next layer's region while stage 2 runs
@@ -340,50 +318,31 @@ __global__ void __launch_bounds__(512, 1)
       dev::mbar_expect_tx(bar, fbytes);
       dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)(x2 + 1), 0);
     }
-    // ---- stage 2: task = (h, s0 tile); sweep the region's y elements ---------
-    for (int t = warp; t < nh * (PTP / 8); t += NW) {
-      const int h = t / (PTP / 8), st = t % (PTP / 8);
-      double* Hh = Hs + h * PTP * GP + st * 8 + 2 * m4;
-      const int g_lo = pl.h_g0[h], g_hi = g_lo + pl.h_ng[h];
-#pragma unroll
-      for (int el = 0; el < ER; ++el) {
-        double d[NLT][2];
-#pragma unroll
-        for (int mt = 0; mt < NLT; ++mt) d[mt][0] = d[mt][1] = 0.0;
+    // ---- stage 2: task = (s1 tile, s0 tile), all stage-2 groups ----------------
+    for (int t = warp; t < (PTP / 8) * (PTP / 8); t += NW) {
+      const int mt = t / (PTP / 8), st = t % (PTP / 8);
+      int k_lo, k_hi;
+      slot_tile_ksteps<P, Q, T>(mt, XRP / 4, k_lo, k_hi);
+      const int s1 = mt * 8 + g8;
+      const int64_t gs1 = (int64_t)a1 * W + s1;
+      const bool row_ok = s1 < PT && gs1 < a.NS1;
+      for (int h = 0; h < nh; ++h) {
+        double d0 = 0.0, d1 = 0.0;
+        const int g_lo = pl.h_g0[h], g_hi = g_lo + pl.h_ng[h];
         for (int g = g_lo; g < g_hi; ++g) {
-          const double* Gg = Gs + g * XRP * GP + (el * Q) * GP + st * 8 + g8;
-          const double* Wg = W1 + (el * 4 + pl.g_v1[g]) * (QP * WP);
-#pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            const int q = ks * 4 + m4;
-            const double bv = q < Q ? Gg[q * GP] : 0.0;
-#pragma unroll
-            for (int mt = 0; mt < NLT; ++mt) dmma_a(d[mt][0], d[mt][1], Wg[q * WP + mt * 8 + g8], bv);
-          }
+          const double* Wg = W1 + pl.g_v1[g] * (PTP * YP) + s1 * YP + m4;
+          const double* Gg = Gs + (g * XRP + m4) * SP + st * 8 + g8;
+          for (int ks = k_lo; ks < k_hi; ++ks) dmma_a(d0, d1, Wg[ks * 4], Gg[ks * 4 * SP]);
         }
-#pragma unroll
-        for (int mt = 0; mt < NLT; ++mt)
-          if (el >= lo2[mt] && el < hi2[mt]) {
-            double2* dst = reinterpret_cast<double2*>(Hh + (el * W + base2[mt]) * GP);
-            double2 v = *dst;
-            v.x += d[mt][0];
-            v.y += d[mt][1];
-            *dst = v;
-          }
-        __syncwarp();
+        if (row_ok) {
+          double* dst = a.H + ((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + (int64_t)a0 * W;
+          const int s0 = st * 8 + 2 * m4;
+          if (s0 < PT && (int64_t)a0 * W + s0 < a.NS0) dst[s0] = d0;
+          if (s0 + 1 < PT && (int64_t)a0 * W + s0 + 1 < a.NS0) dst[s0 + 1] = d1;
+        }
       }
     }
     __syncthreads();
-    // ---- write H[x2][h][s1][s0] for the tile's valid slots -------------------
-    for (int row = warp; row < nh * PT; row += NW) {
-      const int h = row / PT, s1 = row % PT;
-      const int64_t gs1 = (int64_t)a1 * W + s1;
-      if (gs1 >= a.NS1) continue;
-      double* dst = a.H + ((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + (int64_t)a0 * W;
-      const double* src = Hs + (h * PTP + s1) * GP;
-      for (int s0 = lane; s0 < PT; s0 += 32)
-        if ((int64_t)a0 * W + s0 < a.NS0) dst[s0] = src[s0];
-    }
   }
 }
 
@@ -658,16 +617,24 @@ __global__ void __launch_bounds__(128) asm2_stage2(const Asm2bArgs a) {
 
 // ---- host side ----------------------------------------------------------------
 
-constexpr int kTile = 4;
+// Row tile per direction of the 3D stage-1/2 kernel: the largest of 4, 2, 1
+// whose shared-memory plan fits (0 = none).
+template <int P>
+int asm3_tile(const AsmPlan& pl, int nplanes) {
+  if (A3Cfg<P, P, 4>::smem(nplanes, pl.ng) <= 232448) return 4;
+  if (A3Cfg<P, P, 2>::smem(nplanes, pl.ng) <= 232448) return 2;
+  if (A3Cfg<P, P, 1>::smem(nplanes, pl.ng) <= 232448) return 1;
+  return 0;
+}
 
-size_t asm3_smem(int P, const AsmPlan& pl, int nplanes) {
+int asm3_tile_for(int P, const AsmPlan& pl, int nplanes) {
   switch (P) {
-    case 2: return A3Cfg<2, 2, kTile>::smem(nplanes, pl.ng, pl.nh);
-    case 3: return A3Cfg<3, 3, kTile>::smem(nplanes, pl.ng, pl.nh);
-    case 4: return A3Cfg<4, 4, kTile>::smem(nplanes, pl.ng, pl.nh);
-    case 5: return A3Cfg<5, 5, kTile>::smem(nplanes, pl.ng, pl.nh);
-    case 6: return A3Cfg<6, 6, kTile>::smem(nplanes, pl.ng, pl.nh);
-    default: return ~size_t(0);
+    case 2: return asm3_tile<2>(pl, nplanes);
+    case 3: return asm3_tile<3>(pl, nplanes);
+    case 4: return asm3_tile<4>(pl, nplanes);
+    case 5: return asm3_tile<5>(pl, nplanes);
+    case 6: return asm3_tile<6>(pl, nplanes);
+    default: return 0;
   }
 }
 
@@ -706,7 +673,7 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
     }
   if (s.fs.p < 2 || s.fs.p > 6 || s.fs.k != s.fs.p) return false;
   if (d == 3) {
-    if (asm3_smem(s.fs.p, s.plan, p->n_planes) > 232448) return false;  // stage-1/2 tile must fit
+    if (asm3_tile_for(s.fs.p, s.plan, p->n_planes) == 0) return false;  // stage-1/2 tile must fit
     // TMA: 16-byte aligned rows and plane stride
     if ((s.fs.npt[0] * 8) % 16 != 0 || (p->plane_stride * 8) % 16 != 0 || p->n_planes > 256) return false;
   }
@@ -736,10 +703,10 @@ size_t asm_workspace(const AsmShape& s) {
   return (size_t)s.fs.npt[1] * s.plan.ng * (s.fs.nfn[0] * W) * sizeof(double) + 512;
 }
 
-template <int P, int Q>
-igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
-                   const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st) {
-  using C = A3Cfg<P, Q, kTile>;
+template <int P, int Q, int T>
+igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const double* planes, double* H,
+                           cudaStream_t st) {
+  using C = A3Cfg<P, Q, T>;
   Asm3Args a{};
   a.plan = s.plan;
   a.tab = tab_args(p);
@@ -748,10 +715,10 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   a.H = H;
   a.NS0 = s.fs.nfn[0] * C::W;
   a.NS1 = s.fs.nfn[1] * C::W;
-  a.nt0 = (int)ceil_div(s.fs.nfn[0], kTile);
-  a.nt1 = (int)ceil_div(s.fs.nfn[1], kTile);
+  a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
+  a.nt1 = (int)ceil_div(s.fs.nfn[1], T);
   a.nplanes = p->n_planes;
-  size_t smem = C::smem(a.nplanes, s.plan.ng, s.plan.nh);
+  size_t smem = C::smem(a.nplanes, s.plan.ng);
   if (smem > 232448) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
   if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
   CUtensorMap fmap;
@@ -766,15 +733,32 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   if (nz < 1) nz = 1;
   a.lz = (int)ceil_div(s.fs.npt[2], nz);
   if (a.lz < 1) a.lz = 1;
-  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage12<P, Q, kTile>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage12<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem),
                      "smem attribute"));
   dim3 grid((unsigned)tiles, (unsigned)ceil_div(s.fs.npt[2], a.lz));
-  asm3_stage12<P, Q, kTile><<<grid, C::NT, smem, st>>>(a, fmap);  // C::NT = 512
+  asm3_stage12<P, Q, T><<<grid, C::NT, smem, st>>>(a, fmap);
   IGS_LAUNCH_CHECK("asm3_stage12");
+  return IGS_OK;
+}
+
+template <int P, int Q>
+igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
+                   const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st) {
+  switch (asm3_tile<P>(s.plan, p->n_planes)) {
+    case 4: IGS_TRY((launch3_stage12<P, Q, 4>(p, s, planes, H, st))); break;
+    case 2: IGS_TRY((launch3_stage12<P, Q, 2>(p, s, planes, H, st))); break;
+    case 1: IGS_TRY((launch3_stage12<P, Q, 1>(p, s, planes, H, st))); break;
+    default: return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
+  }
+  constexpr int W = 2 * P - 1;
+  struct {
+    int64_t NS0, NS1;
+  } a{s.fs.nfn[0] * W, s.fs.nfn[1] * W};
+  const TabArgs tab = tab_args(p);
   Asm3bArgs b{};
   b.plan = s.plan;
-  b.tab = a.tab;
+  b.tab = tab;
   b.H = H;
   b.NS0 = a.NS0;
   b.NS1 = a.NS1;
