@@ -355,17 +355,61 @@ struct Asm3bArgs {
   int64_t row_lo, row_hi;         // rows to write
   const int64_t* base;            // CSR offset of row_lo (device scalar)
   double* values;
+  const double* w2g;              // [K2][Q][P][P][4] stage-3 weights
 };
 
-// One thread per (slot0, slot1): sweep z with a ring of P rows x (2P-1) cols.
+// W_z^{v2(h)}[jn][jm] at the Q points of every z element, laid out
+// [e2][q][jm][jn][h(4)] (zero for h >= nh): the stage-3 weights, computed once.
 template <int P, int Q>
-__global__ void __launch_bounds__(128) asm3_stage3(const Asm3bArgs a) {
-  constexpr int W = 2 * P - 1;
-  // W_z^{v2(h)}[jn][jm] at the element's Q points, h innermost (zero for h >= nh)
-  __shared__ __align__(16) double w2s[Q][P][P][4];
+__global__ void asm3_w2_kernel(const Asm3bArgs a, double* w2g) {
+  constexpr int NWT = Q * P * P * 4;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)a.tab.K[2] * NWT) return;
+  const int e2 = (int)(i / NWT), r = (int)(i % NWT);
+  const int hh = r % 4, jn = (r / 4) % P, jm = (r / (4 * P)) % P, q = r / (4 * P * P);
+  double val = 0.0;
+  if (hh < a.plan.nh) {
+    const int v = a.plan.h_v2[hh];
+    const int64_t x = (int64_t)e2 * Q + q;
+    const double w = a.tab.wts[2][x];
+    const double bn = (v & 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v & 1) * P + jn) * a.tab.X[2] + x];
+    const double bm = (v >> 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v >> 1) * P + jm) * a.tab.X[2] + x];
+    val = (w * bn) * bm;
+  }
+  w2g[i] = val;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dev::smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Stage-3 pipeline: shared-memory ring of NS3 element stages, prefetched
+// D3 = NS3 - 2 elements ahead with cp.async (no registers held by loads).
+constexpr int NS3 = 4, D3 = NS3 - 2, NT3 = 128;
+template <int P, int Q>
+struct S3Cfg {
+  static constexpr int NWT = Q * P * P * 4;   // weights per element
+  static constexpr int HST = Q * 4 * NT3;     // H values per stage [q][h][thread]
+  static constexpr size_t SMEM = (size_t)NS3 * (HST + NWT) * sizeof(double);
+};
+
+// One thread per (slot0, slot1): sweep z with a ring of P rows x (2P-1) cols
+// in registers.  Each thread streams its own H values (Q points x 4 groups
+// per element) into a private column of the shared stage ring; the element
+// weights stream into the same ring slot, published by one barrier per
+// element, so HBM reads stay D3 elements ahead of the contraction.
+template <int P, int Q>
+__global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bArgs a) {
+  using C = S3Cfg<P, Q>;
+  constexpr int W = 2 * P - 1, NWT = C::NWT;
+  static_assert(NWT % 2 == 0, "16-byte table chunks");
+  extern __shared__ __align__(16) double s3[];
+  double* hst = s3;                    // [NS3][Q][4][NT3]
+  double* w2s = s3 + NS3 * C::HST;     // [NS3][Q][P][P][4]
   const AsmPlan& pl = a.plan;
   const int nh = pl.nh;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t gid = blockIdx.x * (int64_t)NT3 + tid;
   const int64_t s0 = gid % a.NS0, s1 = gid / a.NS0;
   const bool live = s1 < a.NS1;
   const int64_t N0 = a.tab.N[0], N1 = a.tab.N[1], N2 = a.tab.N[2];
@@ -390,7 +434,6 @@ __global__ void __launch_bounds__(128) asm3_stage3(const Asm3bArgs a) {
 #pragma unroll
     for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
   const int K2 = a.tab.K[2];
-  const int nthr = blockDim.x;
   auto flush = [&](int64_t m2, const double* row) {
     const int64_t rp2 = a.pat.rp[2][m2];
     const int64_t w2 = a.pat.rp[2][m2 + 1] - rp2;
@@ -404,63 +447,70 @@ __global__ void __launch_bounds__(128) asm3_stage3(const Asm3bArgs a) {
       if (n2 >= 0 && n2 < N2) a.values[start + (n2 - lo2) * w0 * w1 + r1 * w0 + r0] = row[k];
     }
   };
+  const int64_t hs = a.NS1 * a.NS0;  // stride between (x2, h) planes
+  const double* hbase = a.H + (valid ? s1 * a.NS0 + s0 : 0);
+  // element e2 -> stage e2 % NS3: this thread's H column + its share of the weights
+  auto issue = [&](int e2) {
+    if (e2 < K2) {
+      const int stg = e2 % NS3;
+      const double* hp = hbase + (int64_t)e2 * Q * nh * hs;
+      double* hd = hst + stg * C::HST + tid;
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          const bool ok = valid && hh < nh;
+          const unsigned d = dev::smem_u32(hd + (q * 4 + hh) * NT3);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
+                       "l"(ok ? hp + (q * nh + hh) * hs : a.H), "r"(ok ? 8 : 0)
+                       : "memory");
+        }
+      const double* src = a.w2g + (int64_t)e2 * NWT;
+      double* dst = w2s + stg * NWT;
+      for (int i = tid; i < NWT / 2; i += NT3) cp_async16(dst + 2 * i, src + 2 * i);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per element
+  };
+#pragma unroll
+  for (int e = 0; e < D3; ++e) issue(e);
   for (int eb = 0; eb < K2; eb += P) {
 #pragma unroll
-    for (int r = 0; r < P; ++r) {
+    for (int r = 0; r < P; ++r) {  // ring row of element e2 is static: r
       const int e2 = eb + r;
       if (e2 >= K2) break;
-      __syncthreads();
-      for (int i = threadIdx.x; i < Q * P * P * 4; i += nthr) {
-        const int hh = i % 4, jn = (i / 4) % P, jm = (i / (4 * P)) % P, q = i / (4 * P * P);
-        double val = 0.0;
-        if (hh < nh) {
-          const int v = pl.h_v2[hh];
-          const int64_t x = (int64_t)e2 * Q + q;
-          const double w = a.tab.wts[2][x];
-          const double bn = (v & 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v & 1) * P + jn) * a.tab.X[2] + x];
-          const double bm = (v >> 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v >> 1) * P + jm) * a.tab.X[2] + x];
-          val = (w * bn) * bm;
-        }
-        w2s[q][jm][jn][hh] = val;
-      }
-      __syncthreads();
-      if (valid) {
-        const double* hp = a.H + (int64_t)e2 * Q * nh * a.NS1 * a.NS0 + s1 * a.NS0 + s0;
-        const int64_t hs = a.NS1 * a.NS0;  // stride between (x2, h) planes
-        double h[4], hn[4];
+      // stage (e2 + D3) % NS3 was last read for element e2 - 2, finished by
+      // every thread before the barrier of element e2 - 1
+      issue(e2 + D3);
+      asm volatile("cp.async.wait_group %0;" ::"n"(D3) : "memory");
+      __syncthreads();  // element e2's weights (copied by all threads) visible
+      const int stg = e2 % NS3;
+      const double* hcol = hst + stg * C::HST + tid;
+      const double* wst = w2s + stg * NWT;
 #pragma unroll
-        for (int hh = 0; hh < 4; ++hh) h[hh] = hh < nh ? __ldg(hp + hh * hs) : 0.0;
+      for (int q = 0; q < Q; ++q) {
+        const double h0 = hcol[(q * 4 + 0) * NT3], h1 = hcol[(q * 4 + 1) * NT3];
+        const double h2 = hcol[(q * 4 + 2) * NT3], h3 = hcol[(q * 4 + 3) * NT3];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          if (q + 1 < Q) {  // software pipeline: next point layer's loads in flight
+        for (int jm = 0; jm < P; ++jm)
 #pragma unroll
-            for (int hh = 0; hh < 4; ++hh) hn[hh] = hh < nh ? __ldg(hp + ((q + 1) * nh + hh) * hs) : 0.0;
+          for (int jn = 0; jn < P; ++jn) {
+            const double2 wa = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4);
+            const double2 wb = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4 + 2);
+            double sacc = ring[(r + jm) % P][jn - jm + P - 1];
+            sacc = fma(wa.x, h0, sacc);
+            sacc = fma(wa.y, h1, sacc);
+            sacc = fma(wb.x, h2, sacc);
+            sacc = fma(wb.y, h3, sacc);
+            ring[(r + jm) % P][jn - jm + P - 1] = sacc;
           }
-#pragma unroll
-          for (int jm = 0; jm < P; ++jm)
-#pragma unroll
-            for (int jn = 0; jn < P; ++jn) {
-              const double2 wa = *reinterpret_cast<const double2*>(&w2s[q][jm][jn][0]);
-              const double2 wb = *reinterpret_cast<const double2*>(&w2s[q][jm][jn][2]);
-              double sacc = ring[(r + jm) % P][jn - jm + P - 1];
-              sacc = fma(wa.x, h[0], sacc);
-              sacc = fma(wa.y, h[1], sacc);
-              sacc = fma(wb.x, h[2], sacc);
-              sacc = fma(wb.y, h[3], sacc);
-              ring[(r + jm) % P][jn - jm + P - 1] = sacc;
-            }
-          if (q + 1 < Q) {
-#pragma unroll
-            for (int hh = 0; hh < 4; ++hh) h[hh] = hn[hh];
-          }
-        }
-        // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
-        flush(e2, ring[r % P]);
-#pragma unroll
-        for (int k = 0; k < W; ++k) ring[r % P][k] = 0.0;
       }
+      // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
+      if (valid) flush(e2, ring[r]);
+#pragma unroll
+      for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   // trailing rows m2 in [K2, K2 + P - 1) (their last element is K2 - 1)
   if (valid) {
 #pragma unroll
@@ -698,7 +748,8 @@ TabArgs tab_args(const igs_problem* p) {
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
   if (s.fs.d == 3) {
-    return (size_t)s.fs.npt[2] * s.plan.nh * (s.fs.nfn[1] * W) * (s.fs.nfn[0] * W) * sizeof(double) + 512;
+    return (size_t)s.fs.npt[2] * s.plan.nh * (s.fs.nfn[1] * W) * (s.fs.nfn[0] * W) * sizeof(double) +
+           (size_t)s.fs.nel[2] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
   }
   return (size_t)s.fs.npt[1] * s.plan.ng * (s.fs.nfn[0] * W) * sizeof(double) + 512;
 }
@@ -767,8 +818,20 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.row_hi = row_hi;
   b.values = values;
   b.base = base;
+  // stage-3 weights after H in the workspace
+  double* w2g = H + (size_t)s.fs.npt[2] * s.plan.nh * a.NS1 * a.NS0;
+  b.w2g = w2g;
+  {
+    const int64_t n = (int64_t)tab.K[2] * Q * P * P * 4;
+    asm3_w2_kernel<P, Q><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);
+    IGS_LAUNCH_CHECK("asm3_w2_kernel");
+  }
   int64_t threads = a.NS0 * a.NS1;
-  asm3_stage3<P, Q><<<(unsigned)ceil_div(threads, 128), 128, 0, st>>>(b);
+  constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage3<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem3),
+                     "smem attribute"));
+  asm3_stage3<P, Q><<<(unsigned)ceil_div(threads, NT3), NT3, smem3, st>>>(b);
   IGS_LAUNCH_CHECK("asm3_stage3");
   return IGS_OK;
 }
