@@ -236,12 +236,23 @@ __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row
 // k-steps (of 4 points) of the region that touch the tile rows behind slot
 // tile `st`: row r (tile-relative) is supported by region elements [r, r+P-1].
 template <int P, int Q, int T>
-__device__ __forceinline__ void slot_tile_ksteps(int st, int kmax, int& k_lo, int& k_hi) {
+__host__ __device__ constexpr void slot_tile_ksteps(int st, int kmax, int& k_lo, int& k_hi) {
   constexpr int W = 2 * P - 1;
   const int r_lo = (st * 8) / W;
-  const int r_hi = min(T - 1, (st * 8 + 7) / W);
+  const int r_hi = (st * 8 + 7) / W < T - 1 ? (st * 8 + 7) / W : T - 1;
   k_lo = (r_lo * Q) / 4;
-  k_hi = min(kmax, ((r_hi + P) * Q + 3) / 4);
+  k_hi = ((r_hi + P) * Q + 3) / 4 < kmax ? ((r_hi + P) * Q + 3) / 4 : kmax;
+}
+// longest k-step range over the slot tiles (static unroll bound)
+template <int P, int Q, int T>
+constexpr int max_ksteps(int ntiles, int kmax) {
+  int m = 1;
+  for (int st = 0; st < ntiles; ++st) {
+    int lo = 0, hi = 0;
+    slot_tile_ksteps<P, Q, T>(st, kmax, lo, hi);
+    if (hi - lo > m) m = hi - lo;
+  }
+  return m;
 }
 
 // Per (tile of T x T rows, chunk of z point layers), for every layer, as
@@ -258,6 +269,7 @@ __global__ void __launch_bounds__(512, 1)
   using C = A3Cfg<P, Q, T>;
   constexpr int PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, XK = C::XK;
   constexpr int NT = C::NT, NW = C::NW, SP = C::SP, YP = C::YP, W = C::W;
+  constexpr int KL1 = max_ksteps<P, Q, T>(PTP / 8, XK / 4), KL2 = max_ksteps<P, Q, T>(PTP / 8, XRP / 4);
   extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
   const int ng = pl.ng, nh = pl.nh;
@@ -293,22 +305,31 @@ __global__ void __launch_bounds__(512, 1)
   for (int64_t x2 = z_lo; x2 < z_hi; ++x2, phase ^= 1) {
     dev::mbar_wait(bar, phase);
     // ---- stage 1: task = (y tile, s0 tile), all groups --------------------------
+    // blocks are ordered by group: the accumulator is stored and reset after
+    // the last block of each group (static block index: plan reads are
+    // constant-bank immediates)
     for (int t = warp; t < (XRP / 8) * (PTP / 8); t += NW) {
       const int yt = t / (PTP / 8), st = t % (PTP / 8);
       int k_lo, k_hi;
       slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
       const int y = yt * 8 + g8;
-      for (int g = 0; g < ng; ++g) {
-        double d0 = 0.0, d1 = 0.0;
-        const int b_lo = pl.g_b0[g], b_hi = b_lo + pl.g_nb[g];
-        for (int b = b_lo; b < b_hi; ++b) {
-          const double* Fb = Fs + pl.b_plane[b] * (XRP * XR) + y * XR + m4;
-          const double* Wb = W0 + pl.b_v0[b] * (XK * SP) + m4 * SP + st * 8 + g8;
-          for (int ks = k_lo; ks < k_hi; ++ks) dmma_a(d0, d1, Fb[ks * 4], Wb[ks * 4 * SP]);
+      const double* Fy = Fs + y * XR + m4 + k_lo * 4;
+      const double* Wk = W0 + (m4 + k_lo * 4) * SP + st * 8 + g8;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < kMaxBlocks; ++b) {
+        if (b >= pl.nb) break;
+        const double* Fb = Fy + pl.b_plane[b] * (XRP * XR);
+        const double* Wb = Wk + pl.b_v0[b] * (XK * SP);
+#pragma unroll
+        for (int kk = 0; kk < KL1; ++kk)
+          if (k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
+        if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
+          double* Gd = Gs + (pl.b_g[b] * XRP + y) * SP + st * 8 + 2 * m4;
+          Gd[0] = d0;
+          Gd[1] = d1;
+          d0 = d1 = 0.0;
         }
-        double* Gd = Gs + (g * XRP + y) * SP + st * 8 + 2 * m4;
-        Gd[0] = d0;
-        Gd[1] = d1;
       }
     }
     __syncthreads();
@@ -326,19 +347,26 @@ __global__ void __launch_bounds__(512, 1)
       const int s1 = mt * 8 + g8;
       const int64_t gs1 = (int64_t)a1 * W + s1;
       const bool row_ok = s1 < PT && gs1 < a.NS1;
-      for (int h = 0; h < nh; ++h) {
-        double d0 = 0.0, d1 = 0.0;
-        const int g_lo = pl.h_g0[h], g_hi = g_lo + pl.h_ng[h];
-        for (int g = g_lo; g < g_hi; ++g) {
-          const double* Wg = W1 + pl.g_v1[g] * (PTP * YP) + s1 * YP + m4;
-          const double* Gg = Gs + (g * XRP + m4) * SP + st * 8 + g8;
-          for (int ks = k_lo; ks < k_hi; ++ks) dmma_a(d0, d1, Wg[ks * 4], Gg[ks * 4 * SP]);
-        }
-        if (row_ok) {
-          double* dst = a.H + ((x2 * nh + h) * a.NS1 + gs1) * a.NS0 + (int64_t)a0 * W;
-          const int s0 = st * 8 + 2 * m4;
-          if (s0 < PT && (int64_t)a0 * W + s0 < a.NS0) dst[s0] = d0;
-          if (s0 + 1 < PT && (int64_t)a0 * W + s0 + 1 < a.NS0) dst[s0 + 1] = d1;
+      const int s0 = st * 8 + 2 * m4;
+      const bool ok0 = row_ok && s0 < PT && (int64_t)a0 * W + s0 < a.NS0;
+      const bool ok1 = row_ok && s0 + 1 < PT && (int64_t)a0 * W + s0 + 1 < a.NS0;
+      double* hrow = a.H + (x2 * nh * a.NS1 + gs1) * a.NS0 + (int64_t)a0 * W + s0;
+      const double* Wk = W1 + s1 * YP + m4 + k_lo * 4;
+      const double* Gk = Gs + (m4 + k_lo * 4) * SP + st * 8 + g8;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int g = 0; g < kMaxBlocks; ++g) {
+        if (g >= pl.ng) break;
+        const double* Wg = Wk + pl.g_v1[g] * (PTP * YP);
+        const double* Gg = Gk + g * (XRP * SP);
+#pragma unroll
+        for (int kk = 0; kk < KL2; ++kk)
+          if (k_lo + kk < k_hi) dmma_a(d0, d1, Wg[kk * 4], Gg[kk * 4 * SP]);
+        if (g + 1 == pl.ng || pl.g_h[g + 1] != pl.g_h[g]) {
+          double* dst = hrow + (int64_t)pl.g_h[g] * a.NS1 * a.NS0;
+          if (ok0) dst[0] = d0;
+          if (ok1) dst[1] = d1;
+          d0 = d1 = 0.0;
         }
       }
     }
