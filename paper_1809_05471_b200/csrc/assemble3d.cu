@@ -174,7 +174,10 @@ __device__ __forceinline__ void dmma_a(double& d0, double& d1, double a, double 
 template <int P, int Q, int T>
 struct A3Cfg {
   static constexpr int W = 2 * P - 1;        // band width
-  static constexpr int PT = T * W;           // slots per tile per direction
+  // slot positions per row: a 7-wide band is padded to 8 so every MMA slot
+  // tile is exactly one row (its k-range is then exactly the row's P elements)
+  static constexpr int SR = W == 7 ? 8 : W;
+  static constexpr int PT = T * SR;          // slot positions per tile per direction
   static constexpr int PTP = (PT + 7) & ~7;  // padded to MMA tiles
   static constexpr int ER = T + P - 1;       // elements in the support region
   static constexpr int XR = ER * Q;          // points in the region (TMA box width)
@@ -214,9 +217,9 @@ __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row
     const int col = i % PITCH, row = (i / PITCH) % ROWS, v = i / (PITCH * ROWS);
     const int xl = TRANSPOSED ? col : row, sl = TRANSPOSED ? row : col;
     double val = 0.0;
-    if (xl < C::XR && xl < NX && sl < C::PT && sl < NS) {
+    if (xl < C::XR && xl < NX && sl < C::PT && sl < NS && sl % C::SR < W) {
       const int64_t x = x_first + xl;
-      const int64_t m = a_row + sl / W, n = m + sl % W - (P - 1);
+      const int64_t m = a_row + sl / C::SR, n = m + sl % C::SR - (P - 1);
       if (x >= 0 && x < t.X[dir] && m < Nf && n >= 0 && n < Nf) {
         const int64_t e = x / Q;
         const int64_t jn = n - e, jm = m - e;
@@ -237,9 +240,9 @@ __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row
 // tile `st`: row r (tile-relative) is supported by region elements [r, r+P-1].
 template <int P, int Q, int T>
 __host__ __device__ constexpr void slot_tile_ksteps(int st, int kmax, int& k_lo, int& k_hi) {
-  constexpr int W = 2 * P - 1;
-  const int r_lo = (st * 8) / W;
-  const int r_hi = (st * 8 + 7) / W < T - 1 ? (st * 8 + 7) / W : T - 1;
+  constexpr int SR = A3Cfg<P, Q, T>::SR;
+  const int r_lo = (st * 8) / SR;
+  const int r_hi = (st * 8 + 7) / SR < T - 1 ? (st * 8 + 7) / SR : T - 1;
   k_lo = (r_lo * Q) / 4;
   k_hi = ((r_hi + P) * Q + 3) / 4 < kmax ? ((r_hi + P) * Q + 3) / 4 : kmax;
 }
@@ -344,13 +347,16 @@ __global__ void __launch_bounds__(512, 1)
       const int mt = t / (PTP / 8), st = t % (PTP / 8);
       int k_lo, k_hi;
       slot_tile_ksteps<P, Q, T>(mt, XRP / 4, k_lo, k_hi);
-      const int s1 = mt * 8 + g8;
-      const int64_t gs1 = (int64_t)a1 * W + s1;
-      const bool row_ok = s1 < PT && gs1 < a.NS1;
+      constexpr int SR = C::SR;
+      const int s1 = mt * 8 + g8;  // slot position (row s1 / SR, offset s1 % SR)
+      const int64_t gs1 = (int64_t)(a1 + s1 / SR) * W + s1 % SR;
+      const bool row_ok = s1 < PT && s1 % SR < W && gs1 < a.NS1;
       const int s0 = st * 8 + 2 * m4;
-      const bool ok0 = row_ok && s0 < PT && (int64_t)a0 * W + s0 < a.NS0;
-      const bool ok1 = row_ok && s0 + 1 < PT && (int64_t)a0 * W + s0 + 1 < a.NS0;
-      double* hrow = a.H + (x2 * nh * a.NS1 + gs1) * a.NS0 + (int64_t)a0 * W + s0;
+      const int64_t gs0 = (int64_t)(a0 + s0 / SR) * W + s0 % SR;
+      const int64_t gs0b = (int64_t)(a0 + (s0 + 1) / SR) * W + (s0 + 1) % SR;
+      const bool ok0 = row_ok && s0 < PT && s0 % SR < W && gs0 < a.NS0;
+      const bool ok1 = row_ok && s0 + 1 < PT && (s0 + 1) % SR < W && gs0b < a.NS0;
+      double* hrow = a.H + (x2 * nh * a.NS1 + gs1) * a.NS0;
       const double* Wk = W1 + s1 * YP + m4 + k_lo * 4;
       const double* Gk = Gs + (m4 + k_lo * 4) * SP + st * 8 + g8;
       double d0 = 0.0, d1 = 0.0;
@@ -364,8 +370,8 @@ __global__ void __launch_bounds__(512, 1)
           if (k_lo + kk < k_hi) dmma_a(d0, d1, Wg[kk * 4], Gg[kk * 4 * SP]);
         if (g + 1 == pl.ng || pl.g_h[g + 1] != pl.g_h[g]) {
           double* dst = hrow + (int64_t)pl.g_h[g] * a.NS1 * a.NS0;
-          if (ok0) dst[0] = d0;
-          if (ok1) dst[1] = d1;
+          if (ok0) dst[gs0] = d0;
+          if (ok1) dst[gs0b] = d1;
           d0 = d1 = 0.0;
         }
       }
