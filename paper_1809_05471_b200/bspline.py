@@ -219,8 +219,8 @@ def tabulate(basis, points, max_deriv):
         pts_dev = points.to(device="cuda", dtype=torch.float64).contiguous()
         pts_host = pts_dev.cpu().numpy()
     else:
-        pts_host = np.ascontiguousarray(points, dtype=float)
-        pts_dev = torch.as_tensor(pts_host, device="cuda")
+        pts_host = np.array(points, dtype=float, copy=True)
+        pts_dev = torch.from_numpy(pts_host).to("cuda")
     npts = len(pts_host)
     values = torch.empty((max_deriv + 1, p, npts), dtype=torch.float64, device="cuda")
     first = torch.empty(npts, dtype=torch.int64, device="cuda")
