@@ -141,8 +141,8 @@ class UnivariateBasis:
         t = self._dev.get("csupp")
         if t is None:
             torch = _lib.require_cuda()
-            t = (torch.as_tensor(self.csupp_lo, dtype=torch.float64, device="cuda"),
-                 torch.as_tensor(self.csupp_hi, dtype=torch.float64, device="cuda"))
+            t = (torch.tensor(self.csupp_lo, dtype=torch.float64, device="cuda"),
+                 torch.tensor(self.csupp_hi, dtype=torch.float64, device="cuda"))
             self._dev["csupp"] = t
         return t
 

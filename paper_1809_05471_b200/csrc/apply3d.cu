@@ -319,21 +319,18 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // line / Q at point line % Q): A[g][k] = By_v[line % Q][ynb + k - line / Q]
   // over DoF rows ynb + k, k = m + 4s (zero outside the element's support)
   const int ynb = (wlg * 8) / Q;
-  double byA[2][2], byT[2][2];
+  // (recomputed from the shared Ty table where used: no registers held
+  // across the X sweep)
+  auto y_frag = [&](int v, int s) {
+    const int line = wlg * 8 + g, eyl = line / Q, q1 = line % Q, jj = ynb + m + 4 * s - eyl;
+    return (jj >= 0 && jj < P && (v == 0 || STIFF)) ? Ty[((eyl * 2 + v) * 8 + q1) * 8 + jj] : 0.0;
+  };
+  // transpose: A[k = g][line' = m + 4s] = By_v[line' % Q][ynb + g - line' / Q]
+  auto yt_frag = [&](int v, int s) {
+    const int lt = wlg * 8 + m + 4 * s, eyt = lt / Q, qt = lt % Q, jt = ynb + g - eyt;
+    return (jt >= 0 && jt < P && (v == 0 || STIFF)) ? Ty[((eyt * 2 + v) * 8 + qt) * 8 + jt] : 0.0;
+  };
   __syncthreads();
-  {
-    const int line = wlg * 8 + g, eyl = line / Q, q1 = line % Q;
-#pragma unroll
-    for (int v = 0; v < 2; ++v)
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int jj = ynb + m + 4 * s - eyl;
-        byA[v][s] = (jj >= 0 && jj < P && (v == 0 || STIFF)) ? Ty[((eyl * 2 + v) * 8 + q1) * 8 + jj] : 0.0;
-        // transpose: A[k = g][line' = m + 4s] = By_v[line' % Q][ynb + g - line' / Q]
-        const int lt = wlg * 8 + m + 4 * s, eyt = lt / Q, qt = lt % Q, jt = ynb + g - eyt;
-        byT[v][s] = (jt >= 0 && jt < P && (v == 0 || STIFF)) ? Ty[((eyt * 2 + v) * 8 + qt) * 8 + jt] : 0.0;
-      }
-  }
   for (int n1 = tid; n1 < FY; n1 += NT) {
     int lo = NLG, hi = -1;
     for (int lg = 0; lg < NLG; ++lg) {
@@ -446,6 +443,11 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         // Y for this warp's 8 lines: C_vw[line][n0] = Σ_k By_w[line][k] ·
         // A_v[nb + k][n0] with the banded per-warp fragments byA (k = m + 4s)
         {
+          double byA[2][2];
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) byA[v][s] = y_frag(v, s);
           const double* A0 = Aq + (wq * NA) * LXR + ynb * RP;
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
@@ -635,6 +637,11 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         // S_1 = By0·R01 over DoF rows ynb + k (fragments byT, k = g), stored
         // over the warp's own R rows (planes 0 and 1) once all are consumed
         {
+          double byT[2][2];
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+#pragma unroll
+            for (int s = 0; s < 2; ++s) byT[v][s] = yt_frag(v, s);
           const double* R0 = Cb + (wlg * 8) * RP;
           double d0[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, d1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll

@@ -161,6 +161,8 @@ struct Asm3Args {
   int nt0, nt1;       // row tiles
   int lz;             // z point layers per CTA
   int nplanes;        // planes in the TMA box (all planes of the field)
+  int64_t z0, z1;     // global z points to contract: elements [e_lo, e_hi) of the row range
+  int64_t zpl;        // global z point of the coefficient planes' first layer (slab origin)
 };
 
 __device__ __forceinline__ void dmma_a(double& d0, double& d1, double a, double b) {
@@ -285,8 +287,8 @@ __global__ void __launch_bounds__(512, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, m4 = lane & 3;
   const int t0 = blockIdx.x % a.nt0, t1 = blockIdx.x / a.nt0;
-  const int64_t z_lo = (int64_t)blockIdx.y * a.lz;
-  const int64_t z_hi = min64(a.tab.X[2], z_lo + a.lz);
+  const int64_t z_lo = a.z0 + (int64_t)blockIdx.y * a.lz;
+  const int64_t z_hi = min64(a.z1, z_lo + a.lz);
   const int a0 = t0 * T, a1 = t1 * T;                     // first rows of the tile
   const int xb0 = (a0 - (P - 1)) * Q, xb1 = (a1 - (P - 1)) * Q;  // first region points (may be < 0)
   const unsigned fbytes = (unsigned)((size_t)a.nplanes * XRP * XR * sizeof(double));
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   if (tid == 0 && z_lo < z_hi) {
     dev::mbar_expect_tx(bar, fbytes);
-    dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)z_lo, 0);
+    dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)(z_lo - a.zpl), 0);
   }
   fill_band_table<P, Q, T, false>(W0, a.tab, 0, a0, xb0);
   fill_band_table<P, Q, T, true>(W1, a.tab, 1, a1, xb1);
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(512, 1)
     if (tid == 0 && x2 + 1 < z_hi) {
       dev::fence_proxy_async();
       dev::mbar_expect_tx(bar, fbytes);
-      dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)(x2 + 1), 0);
+      dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)(x2 + 1 - a.zpl), 0);
     }
     // ---- stage 2: task = (s1 tile, s0 tile), all stage-2 groups ----------------
     for (int t = warp; t < (PTP / 8) * (PTP / 8); t += NW) {
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(512, 1)
       const int64_t gs0b = (int64_t)(a0 + (s0 + 1) / SR) * W + (s0 + 1) % SR;
       const bool ok0 = row_ok && s0 < PT && s0 % SR < W && gs0 < a.NS0;
       const bool ok1 = row_ok && s0 + 1 < PT && (s0 + 1) % SR < W && gs0b < a.NS0;
-      double* hrow = a.H + (x2 * nh * a.NS1 + gs1) * a.NS0;
+      double* hrow = a.H + ((x2 - a.z0) * nh * a.NS1 + gs1) * a.NS0;
       const double* Wk = W1 + s1 * YP + m4 + k_lo * 4;
       const double* Gk = Gs + (m4 + k_lo * 4) * SP + st * 8 + g8;
       double d0 = 0.0, d1 = 0.0;
@@ -390,6 +392,7 @@ struct Asm3bArgs {
   const int64_t* base;            // CSR offset of row_lo (device scalar)
   double* values;
   const double* w2g;              // [K2][Q][P][P][4] stage-3 weights
+  int e_lo, e_hi;                 // z elements swept (H holds their points from e_lo·Q)
 };
 
 // W_z^{v2(h)}[jn][jm] at the Q points of every z element, laid out
@@ -484,10 +487,11 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bAr
   const int64_t hs = a.NS1 * a.NS0;  // stride between (x2, h) planes
   const double* hbase = a.H + (valid ? s1 * a.NS0 + s0 : 0);
   // element e2 -> stage e2 % NS3: this thread's H column + its share of the weights
+  const int e_lo = a.e_lo, e_hi = a.e_hi;
   auto issue = [&](int e2) {
-    if (e2 < K2) {
+    if (e2 < e_hi) {
       const int stg = e2 % NS3;
-      const double* hp = hbase + (int64_t)e2 * Q * nh * hs;
+      const double* hp = hbase + (int64_t)(e2 - e_lo) * Q * nh * hs;
       double* hd = hst + stg * C::HST + tid;
 #pragma unroll
       for (int q = 0; q < Q; ++q)
@@ -506,12 +510,14 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bAr
     asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per element
   };
 #pragma unroll
-  for (int e = 0; e < D3; ++e) issue(e);
-  for (int eb = 0; eb < K2; eb += P) {
+  for (int e = 0; e < D3; ++e) issue(e_lo + e);
+  // ring slot of row m2 is (m2 - e_lo) % P; rows before e_lo + P - 1 are
+  // incomplete when e_lo > 0 and lie outside the row range by construction
+  for (int eb = e_lo; eb < e_hi; eb += P) {
 #pragma unroll
     for (int r = 0; r < P; ++r) {  // ring row of element e2 is static: r
       const int e2 = eb + r;
-      if (e2 >= K2) break;
+      if (e2 >= e_hi) break;
       // stage (e2 + D3) % NS3 was last read for element e2 - 2, finished by
       // every thread before the barrier of element e2 - 1
       issue(e2 + D3);
@@ -546,11 +552,11 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bAr
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   // trailing rows m2 in [K2, K2 + P - 1) (their last element is K2 - 1)
-  if (valid) {
+  if (valid && e_hi == K2) {
 #pragma unroll
     for (int t = 1; t < P; ++t) {
       const int64_t m2 = K2 - 1 + t;
-      const int slot = (int)(m2 % P);
+      const int slot = (int)((m2 - e_lo) % P);
 #pragma unroll
       for (int s = 0; s < P; ++s)
         if (s == slot) flush(m2, ring[s]);
@@ -725,12 +731,13 @@ int asm3_tile_for(int P, const AsmPlan& pl, int nplanes) {
 struct AsmShape {
   FusedShape fs;
   AsmPlan plan;
+  int64_t zpts;  // z points held by the coefficient planes (slab or grid)
 };
 
 bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
   AsmShape s;
   if (p->d != 2 && p->d != 3) return false;
-  if (p->slab_lo || p->slab_hi) return false;
+  if ((p->slab_lo || p->slab_hi) && p->d != 3) return false;  // slab assembly: 3D fused only
   const int d = p->d;
   s.fs.d = d;
   s.fs.p = p->trial[0].order;
@@ -749,6 +756,7 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
     s.fs.npt[k] = t.num_points;
   }
   if (!build_plan(p, &s.plan)) return false;
+  s.zpts = (p->slab_lo || p->slab_hi) ? (int64_t)(p->slab_hi - p->slab_lo) * s.fs.k : s.fs.npt[d - 1];
   // tables must hold the derivative levels the blocks use
   for (int k = 0; k < d; ++k)
     if (p->trial[k].max_deriv < 1) {
@@ -782,15 +790,37 @@ TabArgs tab_args(const igs_problem* p) {
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
   if (s.fs.d == 3) {
-    return (size_t)s.fs.npt[2] * s.plan.nh * (s.fs.nfn[1] * W) * (s.fs.nfn[0] * W) * sizeof(double) +
+    return (size_t)s.zpts * s.plan.nh * (s.fs.nfn[1] * W) * (s.fs.nfn[0] * W) * sizeof(double) +
            (size_t)s.fs.nel[2] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
   }
   return (size_t)s.fs.npt[1] * s.plan.ng * (s.fs.nfn[0] * W) * sizeof(double) + 512;
 }
 
+// z elements the row range needs (rows of DoF layers [m2a, m2b] are summed
+// over elements [m2a - P + 1, m2b]) and the slab origin of the planes.
+struct ZRange {
+  int e_lo, e_hi;   // elements to contract
+  int sl, sh;       // elements held by the coefficient planes
+};
+
+igs_status z_range(const igs_problem* p, const AsmShape& s, int64_t row_lo, int64_t row_hi, ZRange* z) {
+  const int P = s.fs.p, K2 = (int)s.fs.nel[2];
+  const int64_t layer = s.fs.nfn[0] * s.fs.nfn[1];
+  const int64_t m2a = row_lo / layer, m2b = (row_hi - 1) / layer;
+  z->e_lo = (int)max64(0, m2a - P + 1);
+  z->e_hi = (int)min64(K2, m2b + 1);
+  const bool slab = p->slab_lo || p->slab_hi;
+  z->sl = slab ? p->slab_lo : 0;
+  z->sh = slab ? p->slab_hi : K2;
+  if (z->e_lo < z->sl || z->e_hi > z->sh)
+    return fail(IGS_EARG, "row range needs coefficient elements outside the slab (elements " +
+                              std::to_string(z->e_lo) + ".." + std::to_string(z->e_hi) + ")");
+  return IGS_OK;
+}
+
 template <int P, int Q, int T>
-igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const double* planes, double* H,
-                           cudaStream_t st) {
+igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const ZRange& z, const double* planes,
+                           double* H, cudaStream_t st) {
   using C = A3Cfg<P, Q, T>;
   Asm3Args a{};
   a.plan = s.plan;
@@ -808,20 +838,23 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const double
   if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
   CUtensorMap fmap;
   {
-    const int64_t dims[4] = {s.fs.npt[0], s.fs.npt[1], s.fs.npt[2], p->n_planes};
+    const int64_t dims[4] = {s.fs.npt[0], s.fs.npt[1], (int64_t)(z.sh - z.sl) * Q, p->n_planes};
     const unsigned box[4] = {(unsigned)C::XR, (unsigned)C::XRP, 1u, (unsigned)p->n_planes};
     IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
   }
+  a.z0 = (int64_t)z.e_lo * Q;
+  a.z1 = (int64_t)z.e_hi * Q;
+  a.zpl = (int64_t)z.sl * Q;
   // z chunks: enough CTAs for ~4 waves at one CTA per SM
   const int64_t tiles = (int64_t)a.nt0 * a.nt1;
   int64_t nz = ceil_div(148 * 4, tiles);
   if (nz < 1) nz = 1;
-  a.lz = (int)ceil_div(s.fs.npt[2], nz);
+  a.lz = (int)ceil_div(a.z1 - a.z0, nz);
   if (a.lz < 1) a.lz = 1;
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage12<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem),
                      "smem attribute"));
-  dim3 grid((unsigned)tiles, (unsigned)ceil_div(s.fs.npt[2], a.lz));
+  dim3 grid((unsigned)tiles, (unsigned)ceil_div(a.z1 - a.z0, a.lz));
   asm3_stage12<P, Q, T><<<grid, C::NT, smem, st>>>(a, fmap);
   IGS_LAUNCH_CHECK("asm3_stage12");
   return IGS_OK;
@@ -830,10 +863,13 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const double
 template <int P, int Q>
 igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
                    const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st) {
+  if (row_hi <= row_lo) return IGS_OK;
+  ZRange z;
+  IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
   switch (asm3_tile<P>(s.plan, p->n_planes)) {
-    case 4: IGS_TRY((launch3_stage12<P, Q, 4>(p, s, planes, H, st))); break;
-    case 2: IGS_TRY((launch3_stage12<P, Q, 2>(p, s, planes, H, st))); break;
-    case 1: IGS_TRY((launch3_stage12<P, Q, 1>(p, s, planes, H, st))); break;
+    case 4: IGS_TRY((launch3_stage12<P, Q, 4>(p, s, z, planes, H, st))); break;
+    case 2: IGS_TRY((launch3_stage12<P, Q, 2>(p, s, z, planes, H, st))); break;
+    case 1: IGS_TRY((launch3_stage12<P, Q, 1>(p, s, z, planes, H, st))); break;
     default: return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
   }
   constexpr int W = 2 * P - 1;
@@ -852,9 +888,11 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.row_hi = row_hi;
   b.values = values;
   b.base = base;
-  // stage-3 weights after H in the workspace
-  double* w2g = H + (size_t)s.fs.npt[2] * s.plan.nh * a.NS1 * a.NS0;
+  // stage-3 weights after H in the workspace (H sized for the slab / grid)
+  double* w2g = H + (size_t)(z.sh - z.sl) * Q * s.plan.nh * a.NS1 * a.NS0;
   b.w2g = w2g;
+  b.e_lo = z.e_lo;
+  b.e_hi = z.e_hi;
   {
     const int64_t n = (int64_t)tab.K[2] * Q * P * P * 4;
     asm3_w2_kernel<P, Q><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);

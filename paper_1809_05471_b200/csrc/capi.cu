@@ -77,10 +77,18 @@ extern "C" igs_status igs_assemble_values(const igs_problem* prob, const int64_t
                                           int64_t row_hi, int32_t block_eta, int32_t block_theta,
                                           const double* planes, double* values, void* ws,
                                           size_t ws_bytes, int32_t flags, void* stream) {
+  // A slab (last-direction elements [slab_lo, slab_hi) held by `planes`)
+  // restricts the coefficient data, not the matrix: rows, columns and the 1D
+  // patterns stay global, and the row range must only need slab elements.
+  const bool slab = prob->slab_lo != 0 || prob->slab_hi != 0;
+  if (slab) {
+    Dims Ds;
+    IGS_TRY(validate_problem(prob, &Ds));
+  }
+  igs_problem g = *prob;
+  g.slab_lo = g.slab_hi = 0;
   Dims D;
-  IGS_TRY(validate_problem(prob, &D));
-  if (prob->slab_lo != 0 || prob->slab_hi != 0)
-    return fail(IGS_EARG, "assembly takes row ranges, not slabs");
+  IGS_TRY(validate_problem(&g, &D));
   int64_t nrows = D.ns[0] * D.ns[1] * D.ns[2];
   if (row_lo < 0 || row_hi < row_lo || row_hi > nrows) return fail(IGS_EARG, "row range");
   if ((block_eta < 0) != (block_theta < 0)) return fail(IGS_EARG, "block indices must both be set");
@@ -91,6 +99,7 @@ extern "C" igs_status igs_assemble_values(const igs_problem* prob, const int64_t
   cudaStream_t s = as_stream(stream);
   if (!(flags & IGS_FLAG_FORCE_GENERIC) && block_eta < 0 && fused_assemble_supported(prob, D))
     return fused_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, planes, values, ws, ws_bytes, s);
+  if (slab) return fail(IGS_ECAPACITY, "slab assembly needs the fused 3D kernels (uniform p = k, full sum)");
   return generic_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, block_eta, block_theta, planes,
                           values, ws, ws_bytes, s);
 }

@@ -10,8 +10,12 @@ layers).  One apply is
 
 The exchanges are point-to-point sends/receives through torch.distributed
 (NCCL over NVLink on GPUs, gloo in the CPU tests), issued as one batched
-group per step.  Each message is (p-1)·N0·N1 doubles.  The assembly needs
-no communication (row blocks are independent) and is not handled here.
+group per step.  Each message is (p-1)·N0·N1 doubles.
+
+The assembly needs no communication (SlabAssembly): rank r owns the rows of
+DoF layers [lo_r, hi_r) of the last direction and reads the coefficients of
+elements [lo_r - p + 1, hi_r) — its slab plus a (p-1)-element halo — and
+writes its contiguous CSR slice; global indptr offsets are closed-form.
 """
 
 import torch
@@ -113,3 +117,43 @@ class ShardedApply:
             y_own.copy_(out)
             return y_own
         return out
+
+
+class SlabAssembly:
+    """One rank's row block of a slab-partitioned assembly (no collective).
+
+    Rows are split by DoF layers of the last direction: rank r owns layers
+    own_layers(r) of `part` (the last rank also the trailing p-1 layers);
+    the coefficient planes it needs are those of elements halo_elements(r).
+    """
+
+    def __init__(self, part, rank):
+        self.part = part
+        self.rank = int(rank)
+
+    def own_layers(self):
+        return self.part.own_layers(self.rank)
+
+    def halo_elements(self):
+        """Elements whose coefficients the rank's rows need: [lo - p + 1, hi)."""
+        lo, hi = self.part.elements(self.rank)
+        return max(0, lo - self.part.p + 1), hi
+
+    def row_range(self, layer_rows):
+        a, b = self.own_layers()
+        return a * layer_rows, b * layer_rows
+
+    def assemble(self, problem):
+        """Values and CSR slice (indptr relative to the slice, indices) of the
+        rank's rows.  `problem` holds the full-grid spaces and a coefficient
+        field on the slab halo_elements() (or on the whole grid)."""
+        from .sumfac import _run_assembly
+
+        pat = problem.pattern()
+        layer_rows = pat.shape[0] // problem.test[-1].num_basis
+        lo, hi = self.row_range(layer_rows)
+        vals = _run_assembly(problem, None, None, None, 0, (lo, hi))
+        bounds = pat.indptr_dev[[lo, hi]].tolist()
+        a, b = int(bounds[0]), int(bounds[1])
+        indptr = pat.indptr_dev[lo: hi + 1] - a
+        return vals[: b - a], indptr, pat.indices_dev[a:b]

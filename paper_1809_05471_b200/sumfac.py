@@ -286,13 +286,18 @@ def block_update_count(problem, theta, eta, dir_order=None):
 
 
 def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
+    """Values of rows [lo, hi) (default: all) in CSR order.  With a slab
+    coefficient field (elements [slab_lo, slab_hi) of the last direction,
+    SURVEY §8(e)) the rows must only need slab elements; the result then
+    holds the range's entries at the front (nnz of the range), as for any
+    row range."""
     torch = _lib.require_cuda()
     lib = _lib.load()
-    if problem.slab is not None:
-        raise ValueError("assembly needs the coefficient field on the whole grid (got a slab field)")
     pat = problem.pattern()
-    prob, keep = problem.struct(dir_order)
+    prob, keep = problem.struct(dir_order, slab=problem.slab)
     nrows = pat.shape[0]
+    if row_range is None and problem.slab is not None:
+        raise ValueError("a slab coefficient field assembles row ranges only (see sharded.SlabAssembly)")
     lo, hi = (0, nrows) if row_range is None else row_range
     values = torch.zeros(pat.nnz, dtype=torch.float64, device="cuda")
     if pat.nnz == 0:

@@ -230,3 +230,43 @@ def test_cg_on_matrix_free_operator_and_matrix_market(cuda, tmp_path):
     assert abs(M - A.to_scipy()).max() == 0.0
     r = M @ x.cpu().numpy() - b.cpu().numpy()
     assert np.linalg.norm(r) / np.linalg.norm(b.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("p,K,kind,world", [(4, 12, 3, 2), (4, 10, 3, 3), (3, 10, 2, 4)])
+def test_slab_assembly_matches_full(cuda, p, K, kind, world):
+    """SURVEY §8(e) assembly partition: each rank assembles its DoF-layer row
+    block from the coefficients of its slab plus a (p-1)-element halo; the
+    concatenated slices are bit-identical to the full assembly."""
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.sharded import SlabAssembly, SlabPartition
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
+
+    bases, quad = workloads.spaces(3, p, K)
+    full_planes = workloads.synthetic_planes(3, list(quad.shape), kind, seed=9)
+    full = AssemblyProblem(bases, bases, quad, workloads.field_from_planes(3, kind, full_planes, quad.shape))
+    A = sumfac.assemble(full)
+    layer_pts = quad.num_points // quad.shape[-1]
+    part = SlabPartition(K, p, world)
+    vals, ptrs, cols = [], [], []
+    for r in range(world):
+        sa = SlabAssembly(part, r)
+        lo, hi = sa.halo_elements()
+        planes = full_planes[:, lo * p * layer_pts: hi * p * layer_pts].contiguous()
+        field = workloads.field_from_planes(3, kind, planes, quad.shape, slab=(lo, hi))
+        v, ip, ix = sa.assemble(AssemblyProblem(bases, bases, quad, field))
+        vals.append(v.cpu().numpy())
+        ptrs.append(ip.cpu().numpy() + (ptrs[-1][-1] if ptrs else 0))
+        cols.append(ix.cpu().numpy())
+    np.testing.assert_array_equal(np.concatenate(vals), A.values_np())
+    indptr = np.concatenate([ptrs[0]] + [q[1:] for q in ptrs[1:]])
+    np.testing.assert_array_equal(indptr, A.pattern.indptr)
+    np.testing.assert_array_equal(np.concatenate(cols), A.pattern.indices)
+    # a row range needing elements outside the slab is rejected
+    sa = SlabAssembly(part, world - 1)
+    lo, hi = sa.halo_elements()
+    planes = full_planes[:, (lo + 1) * p * layer_pts: hi * p * layer_pts].contiguous()
+    field = workloads.field_from_planes(3, kind, planes, quad.shape, slab=(lo + 1, hi))
+    with pytest.raises(ValueError):
+        sa.assemble(AssemblyProblem(bases, bases, quad, field))
+    del torch
