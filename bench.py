@@ -147,36 +147,57 @@ def cpu_baseline(w, min_seconds=10.0, seed=0):
                       f"numpy oracle apply_slab on {cores} threads, {t:.1f} s"}
 
 
-def assembly_section(reps=5, cpu=True, seed=0):
+def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
     """C3 assembly (d=3, p=4, 64^3, mass+stiffness) measured in the same run:
     warm assembly (pattern cached, as the reference caches it), CUDA events,
     nnz/s; roofline against the measured fp64 DMMA peak; CPU baseline = the
-    oracle's independent Kronecker assembly on a reduced mesh (same p)."""
+    oracle's Alg. 1 restatement on a reduced mesh (same p).  With N ranks the
+    rows are split by DoF layers of z (sharded.SlabAssembly): each rank
+    generates the coefficients of its slab plus a (p-1)-element halo and
+    writes its CSR slice, no collective; time = max over ranks."""
     import torch
+    import torch.distributed as dist
 
     from paper_1809_05471_b200 import sumfac, workloads
+    from paper_1809_05471_b200.sharded import SlabAssembly, SlabPartition
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
 
-    prob = workloads.make_problem(3, 4, 64, workloads.MASS_STIFF, seed=seed, max_nnz=1 << 40)
-    A = sumfac.assemble(prob)
+    p, K, kind = 4, 64, workloads.MASS_STIFF
+    bases, quad = workloads.spaces(3, p, K)
+    part = SlabPartition(K, p, world)
+    sa = SlabAssembly(part, rank)
+    e_lo, e_hi = (0, K) if world == 1 else sa.halo_elements()
+    planes = workloads.synthetic_planes(3, list(quad.shape), kind, seed=seed, z_range=(e_lo * p, e_hi * p))
+    field = workloads.field_from_planes(3, kind, planes, quad.shape, slab=None if world == 1 else (e_lo, e_hi))
+    prob = AssemblyProblem(bases, bases, quad, field, max_nnz=1 << 40)
+    run = (lambda: sumfac.assemble(prob)) if world == 1 else (lambda: sa.assemble(prob))
+    run()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        A = sumfac.assemble(prob)
+        run()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    nnz = A.nnz
-    npts = prob.quad.num_points
-    b_alg = 8 * prob.coeff.n_planes * npts + 8 * nnz       # planes read + values written
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    nnz = prob.pattern().nnz
+    npts = quad.num_points
+    b_alg = 8 * field.n_planes * npts + 8 * nnz             # planes read + values written (whole job)
     flops = 2 * 10_390_000_000                                # merged-block MACs (DESIGN.md §3, K3)
-    p64 = 37.15e12                                            # measured DMMA peak (profiles/r01_fp64_peak.txt)
+    p64 = 37.15e12 * world                                    # measured DMMA peak per GPU (profiles/r01_fp64_peak.txt)
     out = {"workload": "C3", "desc": "d3 p4 64^3 mass+stiffness assembly (warm, pattern cached)",
            "value": nnz / (ms / 1e3), "unit": "nnz/s", "ms": ms, "nnz": nnz, "fused": sumfac.fused_path(prob),
+           "partition": f"z DoF-layer row blocks x{world} (slab + (p-1)-element halo, no collective)",
            "roofline": {"bound": "fp64", "achieved_tflops": flops / (ms / 1e3) / 1e12, "peak_tflops": p64 / 1e12,
                         "frac": flops / (ms / 1e3) / p64, "hbm_gbs": b_alg / (ms / 1e3) / 1e9,
                         "alg_bytes": b_alg, "alg_flops": flops}}
-    if cpu:
+    if cpu and rank == 0 and world == 1:
         from oracle import igs_oracle as O
 
         K = 24
@@ -346,9 +367,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w)
     asm = None
-    if rank == 0 and world == 1 and not args.no_assembly:
+    if not args.no_assembly:
         try:
-            asm = assembly_section(cpu=not args.no_cpu_baseline)
+            asm = assembly_section(cpu=not args.no_cpu_baseline, rank=rank, world=world)
         except Exception as exc:  # the apply line must still print
             asm = {"error": repr(exc)}
     if rank == 0:

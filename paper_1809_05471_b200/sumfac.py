@@ -299,8 +299,16 @@ def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
     if row_range is None and problem.slab is not None:
         raise ValueError("a slab coefficient field assembles row ranges only (see sharded.SlabAssembly)")
     lo, hi = (0, nrows) if row_range is None else row_range
-    values = torch.zeros(pat.nnz, dtype=torch.float64, device="cuda")
-    if pat.nnz == 0:
+    if row_range is None:
+        n_out = pat.nnz
+    else:
+        ip = pat.indptr
+        n_out = int(ip[hi] - ip[lo])
+    # the fused kernels write every entry of the range (band zeros included)
+    fused = (block is None and not (flags & _lib.FLAG_FORCE_GENERIC)
+             and lib.igs_fused_path(ctypes.byref(prob), _lib.OP_ASSEMBLE))
+    values = (torch.empty if fused else torch.zeros)(n_out, dtype=torch.float64, device="cuda")
+    if n_out == 0:
         return values
     ws_bytes = lib.igs_workspace_bytes(ctypes.byref(prob), _lib.OP_ASSEMBLE, flags)
     ws = problem._cache.get(("ws_asm", ws_bytes))
