@@ -281,7 +281,18 @@ def main():
         def step(x, y):
             op.apply_device(x, y)
     else:
-        sharded = ShardedApply(part, rank, layer_n, lambda xl, yl: op.apply_device(xl, yl), "cuda")
+        split = None
+        if rank < world - 1 and hi - lo > p - 1:
+            # overlap: interior elements run while the ghost layers arrive
+            cut = hi - p + 1
+            npc = (cut - lo) * p * layer_pts
+            op_int = matfree.MatrixFreeOperator(AssemblyProblem(
+                bases, bases, quad, workloads.field_from_planes(d, kind, planes[:, :npc], quad.shape, slab=(lo, cut))))
+            op_bnd = matfree.MatrixFreeOperator(AssemblyProblem(
+                bases, bases, quad, workloads.field_from_planes(d, kind, planes[:, npc:], quad.shape, slab=(cut, hi))))
+            split = (lambda xv, yv: op_int.apply_device(xv, yv),
+                     lambda xv, yv: op_bnd.apply_device(xv, yv, accumulate=True))
+        sharded = ShardedApply(part, rank, layer_n, lambda xl, yl: op.apply_device(xl, yl), "cuda", split=split)
 
         def step(x, y):
             sharded.apply(x, y)

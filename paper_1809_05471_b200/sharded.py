@@ -65,11 +65,17 @@ class ShardedApply:
     MatrixFreeOperator(problem, slab=...).apply_device, or the CPU oracle.
     """
 
-    def __init__(self, part, rank, layer_size, compute, device, dtype=torch.float64, group=None):
+    def __init__(self, part, rank, layer_size, compute, device, dtype=torch.float64, group=None, split=None):
+        """split=(interior, boundary): optional overlap of the ghost gather
+        with compute.  interior(x, y) writes y over DoF layers [lo, hi) from
+        elements [lo, hi-p+1) (own x only); boundary(x, y) ADDS elements
+        [hi-p+1, hi) into DoF layers [hi-p+1, hi+p-1) (needs the ghosts).
+        Both get views starting at their first DoF layer."""
         self.part = part
         self.rank = int(rank)
         self.layer = int(layer_size)
         self.compute = compute
+        self.split = split
         self.group = group
         lo, hi = part.local_layers(self.rank)
         olo, ohi = part.own_layers(self.rank)
@@ -80,15 +86,17 @@ class ShardedApply:
         self.y_local = torch.zeros(self.n_local, dtype=dtype, device=device)
         self.halo_in = torch.zeros((part.p - 1) * self.layer, dtype=dtype, device=device)
 
-    def _exchange(self, send, recv):
+    def _start(self, send, recv):
         ops = []
         for buf, peer in send:
             ops.append(dist.P2POp(dist.isend, buf, peer, group=self.group))
         for buf, peer in recv:
             ops.append(dist.P2POp(dist.irecv, buf, peer, group=self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def _exchange(self, send, recv):
+        for req in self._start(send, recv):
+            req.wait()
 
     def apply(self, x_own, y_own=None):
         """y_own = (A x) restricted to this rank's own DoF layers."""
@@ -100,9 +108,23 @@ class ShardedApply:
             send.append((self.x_local[:g].clone() if self.x_local.device.type == "cpu" else self.x_local[:g], r - 1))
         if r < W - 1 and g:
             recv.append((self.x_local[self.n_own:], r + 1))
-        self._exchange(send, recv)
-        # 2. local apply on the slab
-        self.compute(self.x_local, self.y_local)
+        lo, hi = self.part.elements(r)
+        p = self.part.p
+        if self.split is not None and r < W - 1 and hi - lo > p - 1:
+            # 2a. interior elements while the ghosts are in flight
+            reqs = self._start(send, recv)
+            interior, boundary = self.split
+            interior(self.x_local[: self.n_own], self.y_local[: self.n_own])
+            for req in reqs:
+                req.wait()
+            # 2b. the last p-1 elements need the ghost layers
+            b0 = (hi - lo - p + 1) * self.layer
+            self.y_local[self.n_own:].zero_()
+            boundary(self.x_local[b0:], self.y_local[b0:])
+        else:
+            self._exchange(send, recv)
+            # 2. local apply on the slab
+            self.compute(self.x_local, self.y_local)
         # 3. ghost reduce: my trailing p-1 partial layers go to r+1.
         send, recv = [], []
         if r < W - 1 and g:

@@ -270,3 +270,40 @@ def test_slab_assembly_matches_full(cuda, p, K, kind, world):
     with pytest.raises(ValueError):
         sa.assemble(AssemblyProblem(bases, bases, quad, field))
     del torch
+
+
+@pytest.mark.parametrize("p,kind", [(6, 2), (8, 3), (4, 3)])
+def test_slab_interior_boundary_split_equals_slab_apply(cuda, p, kind):
+    """The overlapped multi-GPU step computes a rank's slab as interior
+    elements [lo, hi-p+1) (own x only) plus boundary elements [hi-p+1, hi)
+    accumulated after the ghosts land; on planes views of one slab this
+    must equal the slab apply."""
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
+
+    K, lo, hi = 16, 3, 13
+    bases, quad = workloads.spaces(3, p, K)
+    layer_pts = quad.num_points // quad.shape[-1]
+    planes = workloads.synthetic_planes(3, list(quad.shape), kind, seed=6, z_range=(lo * p, hi * p))
+
+    def op_on(a, b):
+        view = planes[:, (a - lo) * p * layer_pts: (b - lo) * p * layer_pts]
+        field = workloads.field_from_planes(3, kind, view, quad.shape, slab=(a, b))
+        op = matfree.MatrixFreeOperator(AssemblyProblem(bases, bases, quad, field))
+        assert op.fused
+        return op
+
+    layer_n = int(np.prod([b.num_basis for b in bases[:-1]]))
+    n_loc = (hi - lo + p - 1) * layer_n
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(n_loc, dtype=torch.float64, device="cuda", generator=gen)
+    y_ref = op_on(lo, hi).apply_device(x)
+    cut = hi - p + 1
+    y = torch.zeros(n_loc, dtype=torch.float64, device="cuda")
+    n_own = (hi - lo) * layer_n
+    op_on(lo, cut).apply_device(x[:n_own], y[:n_own])
+    b0 = (cut - lo) * layer_n
+    op_on(cut, hi).apply_device(x[b0:], y[b0:], accumulate=True)
+    err = float(torch.linalg.vector_norm(y - y_ref) / torch.linalg.vector_norm(y_ref))
+    assert err <= 1e-13

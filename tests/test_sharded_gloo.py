@@ -25,7 +25,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, d, p, K, kind, q):
+def _worker(rank, world, port, d, p, K, kind, q, split=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -49,7 +49,19 @@ def _worker(rank, world, port, d, p, K, kind, q):
         full[lo * layer_n: lo * layer_n + xl.numel()] = xl.numpy()
         yl.copy_(torch.from_numpy(O.apply_slab(sp, p, ths, ths, pm, planes, full, lo, hi)))
 
-    sa = ShardedApply(part, rank, layer_n, compute, "cpu")
+    def sub_apply(e0, e1, xv):
+        full = np.zeros(n)
+        full[e0 * layer_n: e0 * layer_n + xv.numel()] = xv.numpy()
+        sub = planes[:, (e0 - lo) * p * layer_x: (e1 - lo) * p * layer_x]
+        return torch.from_numpy(O.apply_slab(sp, p, ths, ths, pm, sub, full, e0, e1))
+
+    def interior(xv, yv):
+        yv.copy_(sub_apply(lo, hi - p + 1, xv))
+
+    def boundary(xv, yv):
+        yv += sub_apply(hi - p + 1, hi, xv)
+
+    sa = ShardedApply(part, rank, layer_n, compute, "cpu", split=(interior, boundary) if split else None)
     olo, ohi = part.own_layers(rank)
     x_own = torch.from_numpy(x[olo * layer_n: ohi * layer_n].copy())
     y_own = sa.apply(x_own).clone()
@@ -62,12 +74,16 @@ def _worker(rank, world, port, d, p, K, kind, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,d,p,K,kind", [(2, 3, 4, 7, 3), (3, 3, 3, 9, 2), (2, 2, 5, 8, 3)])
-def test_sharded_apply_matches_single_process(world, d, p, K, kind):
+@pytest.mark.parametrize("world,d,p,K,kind,split", [(2, 3, 4, 7, 3, False), (3, 3, 3, 9, 2, False),
+                                                   (2, 2, 5, 8, 3, False), (3, 3, 3, 12, 3, True),
+                                                   (2, 2, 5, 11, 2, True)])
+def test_sharded_apply_matches_single_process(world, d, p, K, kind, split):
+    """split=True: interior elements are computed while the ghost gather is in
+    flight, the last p-1 elements after it lands (SURVEY §8(e) overlap)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, d, p, K, kind, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, p, K, kind, q, split)) for r in range(world)]
     for pr in procs:
         pr.start()
     gathered = q.get(timeout=240)
