@@ -18,9 +18,9 @@
 //   3D: asm3_stage12 (per point layer z, tile of 4x4 rows in (x, y)):
 //         G_g[pair0][y] = Σ_{blocks b in g} Σ_x W_x^{v0(b)} F_b      (smem)
 //         H_h[pair1][pair0] = Σ_{g in h} Σ_y W_y^{v1(g)} G_g       -> HBM
-//       asm3_stage3 (one thread per (pair0, pair1)):
+//       asm_sweep<3> (one thread per (pair0, pair1)):
 //         ring[m2][n2] += Σ_h W_z^{v2(h)} H_h  ->  CSR
-//   2D: asm2_stage1 (x) -> HBM, asm2_stage2 (y ring, chunked) -> CSR.
+//   2D: asm2_stage1 (x) -> HBM, asm_sweep<2> (y ring, chunked) -> CSR.
 #include "fused.cuh"
 #include "tma.cuh"
 
@@ -215,7 +215,7 @@ __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row
   constexpr int ROWS = TRANSPOSED ? C::PTP : C::XK;
   constexpr int TOT = 4 * ROWS * PITCH;
   const int64_t Nf = t.N[dir];
-  for (int i = threadIdx.x; i < TOT; i += C::NT) {
+  for (int i = threadIdx.x; i < TOT; i += blockDim.x) {
     const int col = i % PITCH, row = (i / PITCH) % ROWS, v = i / (PITCH * ROWS);
     const int xl = TRANSPOSED ? col : row, sl = TRANSPOSED ? row : col;
     double val = 0.0;
@@ -391,26 +391,30 @@ struct Asm3bArgs {
   int64_t row_lo, row_hi;         // rows to write
   const int64_t* base;            // CSR offset of row_lo (device scalar)
   double* values;
-  const double* w2g;              // [K2][Q][P][P][4] stage-3 weights
-  int e_lo, e_hi;                 // z elements swept (H holds their points from e_lo·Q)
+  const double* w2g;              // [K][Q][P][P][4] weights of the swept direction
+  int e_lo, e_hi;                 // elements swept (H holds their points from e_lo·Q)
+  int chunk;                      // elements per thread chunk (rows written per chunk)
+  int ngrp;                       // groups summed per point (3D: nh, 2D: ng)
+  int grp_v[4];                   // their variant codes in the swept direction
 };
 
-// W_z^{v2(h)}[jn][jm] at the Q points of every z element, laid out
-// [e2][q][jm][jn][h(4)] (zero for h >= nh): the stage-3 weights, computed once.
-template <int P, int Q>
-__global__ void asm3_w2_kernel(const Asm3bArgs a, double* w2g) {
-  constexpr int NWT = Q * P * P * 4;
+// W^{v(h)}[jn][jm] of the swept (last) direction at the Q points of every
+// element, laid out [e][q][jm][jn][h(4)] (zero for h >= ngrp): the last
+// stage's weights, computed once.
+template <int P, int Q, int D>
+__global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
+  constexpr int NWT = Q * P * P * 4, L = D - 1;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)a.tab.K[2] * NWT) return;
+  if (i >= (int64_t)a.tab.K[L] * NWT) return;
   const int e2 = (int)(i / NWT), r = (int)(i % NWT);
   const int hh = r % 4, jn = (r / 4) % P, jm = (r / (4 * P)) % P, q = r / (4 * P * P);
   double val = 0.0;
-  if (hh < a.plan.nh) {
-    const int v = a.plan.h_v2[hh];
+  if (hh < a.ngrp) {
+    const int v = a.grp_v[hh];
     const int64_t x = (int64_t)e2 * Q + q;
-    const double w = a.tab.wts[2][x];
-    const double bn = (v & 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v & 1) * P + jn) * a.tab.X[2] + x];
-    const double bm = (v >> 1) > a.tab.md[2] ? 0.0 : a.tab.vals[2][((int64_t)(v >> 1) * P + jm) * a.tab.X[2] + x];
+    const double w = a.tab.wts[L][x];
+    const double bn = (v & 1) > a.tab.md[L] ? 0.0 : a.tab.vals[L][((int64_t)(v & 1) * P + jn) * a.tab.X[L] + x];
+    const double bm = (v >> 1) > a.tab.md[L] ? 0.0 : a.tab.vals[L][((int64_t)(v >> 1) * P + jm) * a.tab.X[L] + x];
     val = (w * bn) * bm;
   }
   w2g[i] = val;
@@ -430,51 +434,64 @@ struct S3Cfg {
   static constexpr size_t SMEM = (size_t)NS3 * (HST + NWT) * sizeof(double);
 };
 
-// One thread per (slot0, slot1): sweep z with a ring of P rows x (2P-1) cols
-// in registers.  Each thread streams its own H values (Q points x 4 groups
-// per element) into a private column of the shared stage ring; the element
-// weights stream into the same ring slot, published by one barrier per
-// element, so HBM reads stay D3 elements ahead of the contraction.
-template <int P, int Q>
-__global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bArgs a) {
+// Last-direction sweep (3D stage 3, 2D stage 2).  One thread per (slot0[,
+// slot1], chunk of elements) sweeps the last direction with a ring of P rows
+// x (2P-1) cols in registers.  Each thread streams its own H values (Q
+// points x 4 groups per element) into a private column of the shared stage
+// ring; the element weights stream into the same ring slot, published by one
+// barrier per element, so HBM reads stay D3 elements ahead of the
+// contraction.  A chunk starts P-1 elements early (its first rows are then
+// complete) and writes the rows of its own elements (the last chunk also the
+// trailing P-1 rows).  2D is 3D with a trivial middle direction.
+template <int P, int Q, int D>
+__global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs a) {
   using C = S3Cfg<P, Q>;
-  constexpr int W = 2 * P - 1, NWT = C::NWT;
+  constexpr int W = 2 * P - 1, NWT = C::NWT, L = D - 1;
   static_assert(NWT % 2 == 0, "16-byte table chunks");
   extern __shared__ __align__(16) double s3[];
   double* hst = s3;                    // [NS3][Q][4][NT3]
   double* w2s = s3 + NS3 * C::HST;     // [NS3][Q][P][P][4]
-  const AsmPlan& pl = a.plan;
-  const int nh = pl.nh;
+  const int nh = a.ngrp;
   const int tid = threadIdx.x;
   const int64_t gid = blockIdx.x * (int64_t)NT3 + tid;
-  const int64_t s0 = gid % a.NS0, s1 = gid / a.NS0;
-  const bool live = s1 < a.NS1;
-  const int64_t N0 = a.tab.N[0], N1 = a.tab.N[1], N2 = a.tab.N[2];
+  const int64_t npairs = a.NS0 * a.NS1;
+  const int64_t sp = gid % npairs, chunk_id = gid / npairs;
+  const int64_t s0 = sp % a.NS0, s1 = sp / a.NS0;
+  const int nchunk = (a.e_hi - a.e_lo + a.chunk - 1) / a.chunk;
+  const bool live = chunk_id < nchunk;
+  const int64_t N0 = a.tab.N[0], N1 = D == 3 ? a.tab.N[1] : 1, N2 = a.tab.N[L];
   const int64_t m0 = s0 / W, n0 = m0 + (s0 % W) - (P - 1);
-  const int64_t m1 = live ? s1 / W : 0, n1 = m1 + (live ? (s1 % W) : 0) - (P - 1);
+  const int64_t m1 = D == 3 ? s1 / W : 0, n1 = D == 3 ? m1 + (s1 % W) - (P - 1) : 0;
   const bool valid = live && n0 >= 0 && n0 < N0 && n1 >= 0 && n1 < N1 && m0 < N0 && m1 < N1;
-  // CSR geometry of this thread's (row, column) pairs in directions 0, 1
+  // CSR geometry of this thread's (row, column) pairs in the first directions
   int64_t w0 = 1, w1 = 1, rp0 = 0, rp1 = 0, r0 = 0, r1 = 0, P0 = 1, P1 = 1;
   if (valid) {
     rp0 = a.pat.rp[0][m0];
     w0 = a.pat.rp[0][m0 + 1] - rp0;
-    rp1 = a.pat.rp[1][m1];
-    w1 = a.pat.rp[1][m1 + 1] - rp1;
     P0 = a.pat.rp[0][N0];
-    P1 = a.pat.rp[1][N1];
     r0 = n0 - a.pat.cl[0][rp0];
-    r1 = n1 - a.pat.cl[1][rp1];
+    if (D == 3) {
+      rp1 = a.pat.rp[1][m1];
+      w1 = a.pat.rp[1][m1 + 1] - rp1;
+      P1 = a.pat.rp[1][N1];
+      r1 = n1 - a.pat.cl[1][rp1];
+    }
   }
   double ring[P][W];
 #pragma unroll
   for (int r = 0; r < P; ++r)
 #pragma unroll
     for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
-  const int K2 = a.tab.K[2];
+  const int K2 = a.tab.K[L];
+  // this chunk's elements [c_lo, c_hi) and rows [c_lo, c_hi) (+ trailing rows)
+  const int c_lo = a.e_lo + (live ? (int)chunk_id : 0) * a.chunk;
+  const int c_hi = min(a.e_hi, c_lo + a.chunk);
+  const int e_lo = max(a.e_lo, c_lo - (P - 1)), e_hi = c_hi;
   auto flush = [&](int64_t m2, const double* row) {
-    const int64_t rp2 = a.pat.rp[2][m2];
-    const int64_t w2 = a.pat.rp[2][m2 + 1] - rp2;
-    const int64_t lo2 = a.pat.cl[2][rp2];
+    if (m2 < c_lo || (m2 >= c_hi && c_hi != K2)) return;
+    const int64_t rp2 = a.pat.rp[L][m2];
+    const int64_t w2 = a.pat.rp[L][m2 + 1] - rp2;
+    const int64_t lo2 = a.pat.cl[L][rp2];
     const int64_t m = m0 + N0 * (m1 + N1 * m2);
     if (m < a.row_lo || m >= a.row_hi) return;
     const int64_t start = rp0 * w1 * w2 + P0 * rp1 * w2 + P0 * P1 * rp2 - *a.base;
@@ -484,68 +501,78 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bAr
       if (n2 >= 0 && n2 < N2) a.values[start + (n2 - lo2) * w0 * w1 + r1 * w0 + r0] = row[k];
     }
   };
-  const int64_t hs = a.NS1 * a.NS0;  // stride between (x2, h) planes
-  const double* hbase = a.H + (valid ? s1 * a.NS0 + s0 : 0);
-  // element e2 -> stage e2 % NS3: this thread's H column + its share of the weights
-  const int e_lo = a.e_lo, e_hi = a.e_hi;
+  const int64_t hs = npairs;  // stride between (point, group) planes
+  const double* hbase = a.H + (valid ? sp : 0);
+  // The block's threads share one chunk range except at chunk boundaries
+  // inside the block: the stage ring, the weights and the barriers follow
+  // the block-wide range [blk_lo, blk_hi); a thread copies and contracts H
+  // only for the elements of its own range [e_lo, e_hi).
+  const int64_t gid0 = blockIdx.x * (int64_t)NT3, gid1 = gid0 + NT3 - 1;
+  const int cb0 = (int)min64(gid0 / npairs, nchunk - 1), cb1 = (int)min64(gid1 / npairs, nchunk - 1);
+  const int blk_lo = max(a.e_lo, a.e_lo + cb0 * a.chunk - (P - 1));
+  const int blk_hi = min(a.e_hi, a.e_lo + (cb1 + 1) * a.chunk);
+  // element e2 -> stage (e2 - blk_lo) % NS3: this thread's H column + its share of the weights
   auto issue = [&](int e2) {
-    if (e2 < e_hi) {
-      const int stg = e2 % NS3;
-      const double* hp = hbase + (int64_t)(e2 - e_lo) * Q * nh * hs;
-      double* hd = hst + stg * C::HST + tid;
+    if (e2 < blk_hi) {
+      const int stg = (e2 - blk_lo) % NS3;
+      if (e2 >= e_lo && e2 < e_hi) {
+        const double* hp = hbase + (int64_t)(e2 - a.e_lo) * Q * nh * hs;
+        double* hd = hst + stg * C::HST + tid;
 #pragma unroll
-      for (int q = 0; q < Q; ++q)
+        for (int q = 0; q < Q; ++q)
 #pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
-          const bool ok = valid && hh < nh;
-          const unsigned d = dev::smem_u32(hd + (q * 4 + hh) * NT3);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
-                       "l"(ok ? hp + (q * nh + hh) * hs : a.H), "r"(ok ? 8 : 0)
-                       : "memory");
-        }
+          for (int hh = 0; hh < 4; ++hh) {
+            const bool ok = valid && hh < nh;
+            const unsigned d = dev::smem_u32(hd + (q * 4 + hh) * NT3);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
+                         "l"(ok ? hp + (q * nh + hh) * hs : a.H), "r"(ok ? 8 : 0)
+                         : "memory");
+          }
+      }
       const double* src = a.w2g + (int64_t)e2 * NWT;
       double* dst = w2s + stg * NWT;
       for (int i = tid; i < NWT / 2; i += NT3) cp_async16(dst + 2 * i, src + 2 * i);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per element
   };
+  // rebase the ring so slot (m2 - blk_lo) % P is static per unrolled step
 #pragma unroll
-  for (int e = 0; e < D3; ++e) issue(e_lo + e);
-  // ring slot of row m2 is (m2 - e_lo) % P; rows before e_lo + P - 1 are
-  // incomplete when e_lo > 0 and lie outside the row range by construction
-  for (int eb = e_lo; eb < e_hi; eb += P) {
+  for (int e = 0; e < D3; ++e) issue(blk_lo + e);
+  for (int eb = blk_lo; eb < blk_hi; eb += P) {
 #pragma unroll
     for (int r = 0; r < P; ++r) {  // ring row of element e2 is static: r
       const int e2 = eb + r;
-      if (e2 >= e_hi) break;
-      // stage (e2 + D3) % NS3 was last read for element e2 - 2, finished by
-      // every thread before the barrier of element e2 - 1
+      if (e2 >= blk_hi) break;
+      // stage (e2 + D3 - blk_lo) % NS3 was last read for element e2 - 2,
+      // finished by every thread before the barrier of element e2 - 1
       issue(e2 + D3);
       asm volatile("cp.async.wait_group %0;" ::"n"(D3) : "memory");
-      __syncthreads();  // element e2's weights (copied by all threads) visible
-      const int stg = e2 % NS3;
-      const double* hcol = hst + stg * C::HST + tid;
-      const double* wst = w2s + stg * NWT;
+      __syncthreads();  // element e2's weights (copied by the threads that own it) visible
+      if (e2 >= e_lo && e2 < e_hi) {
+        const int stg = (e2 - blk_lo) % NS3;
+        const double* hcol = hst + stg * C::HST + tid;
+        const double* wst = w2s + stg * NWT;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const double h0 = hcol[(q * 4 + 0) * NT3], h1 = hcol[(q * 4 + 1) * NT3];
-        const double h2 = hcol[(q * 4 + 2) * NT3], h3 = hcol[(q * 4 + 3) * NT3];
+        for (int q = 0; q < Q; ++q) {
+          const double h0 = hcol[(q * 4 + 0) * NT3], h1 = hcol[(q * 4 + 1) * NT3];
+          const double h2 = hcol[(q * 4 + 2) * NT3], h3 = hcol[(q * 4 + 3) * NT3];
 #pragma unroll
-        for (int jm = 0; jm < P; ++jm)
+          for (int jm = 0; jm < P; ++jm)
 #pragma unroll
-          for (int jn = 0; jn < P; ++jn) {
-            const double2 wa = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4);
-            const double2 wb = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4 + 2);
-            double sacc = ring[(r + jm) % P][jn - jm + P - 1];
-            sacc = fma(wa.x, h0, sacc);
-            sacc = fma(wa.y, h1, sacc);
-            sacc = fma(wb.x, h2, sacc);
-            sacc = fma(wb.y, h3, sacc);
-            ring[(r + jm) % P][jn - jm + P - 1] = sacc;
-          }
+            for (int jn = 0; jn < P; ++jn) {
+              const double2 wa = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4);
+              const double2 wb = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4 + 2);
+              double sacc = ring[(r + jm) % P][jn - jm + P - 1];
+              sacc = fma(wa.x, h0, sacc);
+              sacc = fma(wa.y, h1, sacc);
+              sacc = fma(wb.x, h2, sacc);
+              sacc = fma(wb.y, h3, sacc);
+              ring[(r + jm) % P][jn - jm + P - 1] = sacc;
+            }
+        }
+        // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
+        if (valid) flush(e2, ring[r]);
       }
-      // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
-      if (valid) flush(e2, ring[r]);
 #pragma unroll
       for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
     }
@@ -556,7 +583,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bAr
 #pragma unroll
     for (int t = 1; t < P; ++t) {
       const int64_t m2 = K2 - 1 + t;
-      const int slot = (int)((m2 - e_lo) % P);
+      const int slot = (int)((m2 - blk_lo) % P);
 #pragma unroll
       for (int s = 0; s < P; ++s)
         if (s == slot) flush(m2, ring[s]);
@@ -569,138 +596,100 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm3_stage3(const Asm3bAr
 struct Asm2Args {
   AsmPlan plan;
   TabArgs tab;
-  const double* planes;
-  int64_t pstride;
-  double* G;     // [X1][ng][NS0]
+  double* G;       // [X1][ng][NS0]
   int64_t NS0;
+  int nt0;         // row tiles in x
+  int yc;          // y points per CTA (multiple of A2_YS)
 };
 
-// G_g[y][s0] = Σ_b∈g Σ_x W0^{v0(b)}[pair0(s0)][x] F_b[y][x]
-template <int P, int Q>
-__global__ void __launch_bounds__(256) asm2_stage1(const Asm2Args a) {
-  constexpr int W = 2 * P - 1;
-  const AsmPlan& pl = a.plan;
-  const int64_t X0 = a.tab.X[0], X1 = a.tab.X[1];
-  const int64_t total = a.NS0 * X1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s0 = i % a.NS0, y = i / a.NS0;
-    const int64_t m0 = s0 / W, n0 = m0 + (s0 % W) - (P - 1);
-    double acc[kMaxBlocks];
-    for (int g = 0; g < pl.ng; ++g) acc[g] = 0.0;
-    if (n0 >= 0 && n0 < a.tab.N[0]) {
-      int64_t elo = (m0 > n0 ? m0 : n0) - (P - 1), ehi = m0 < n0 ? m0 : n0;
-      if (elo < 0) elo = 0;
-      if (ehi > a.tab.K[0] - 1) ehi = a.tab.K[0] - 1;
-      for (int64_t e = elo; e <= ehi; ++e)
-        for (int q = 0; q < Q; ++q) {
-          const int64_t x = e * Q + q;
-          const double w = a.tab.wts[0][x];
-          const double bn0 = bval<P, Q>(a.tab, 0, 0, n0, x), bn1 = bval<P, Q>(a.tab, 0, 1, n0, x);
-          const double bm0 = bval<P, Q>(a.tab, 0, 0, m0, x), bm1 = bval<P, Q>(a.tab, 0, 1, m0, x);
-          const double wv[4] = {(w * bn0) * bm0, (w * bn1) * bm0, (w * bn0) * bm1, (w * bn1) * bm1};
-          for (int b = 0; b < pl.nb; ++b)
-            acc[pl.b_g[b]] = fma(wv[pl.b_v0[b]], __ldg(a.planes + (int64_t)pl.b_plane[b] * a.pstride + y * X0 + x),
-                                 acc[pl.b_g[b]]);
-        }
-    }
-    for (int g = 0; g < pl.ng; ++g) a.G[(y * pl.ng + g) * a.NS0 + s0] = acc[g];
-  }
-}
-
-struct Asm2bArgs {
-  AsmPlan plan;
-  TabArgs tab;
-  const double* G;
-  int64_t NS0;
-  int chunk;         // elements of direction 1 per thread chunk
-  TensorPat pat;
-  int64_t row_lo, row_hi;
-  const int64_t* base;
-  double* values;
+// 2D stage 1 as a dense banded GEMM on DMMA (the 3D stage-1 structure):
+// one CTA per (T-row tile in x, chunk of y points); the tile's band table
+// W0[v][x][slot] is built once and reused for every y block; coefficient
+// boxes of A2_YS y rows x the tile's x region (all planes) stream in by
+// TMA, double-buffered.  G_g[y][s0] = Σ_{b∈g} Σ_x F_b[y][x] W0^{v0(b)}[x][s0].
+constexpr int A2_YS = 64, A2_NT = 256, A2_NW = 8;
+template <int P, int Q, int T>
+struct A2Cfg {
+  using B = A3Cfg<P, Q, T>;
+  static constexpr size_t fbox(int npl) { return ((size_t)npl * A2_YS * B::XR + 4 + 15) & ~size_t(15); }
+  static constexpr size_t smem(int npl) { return (2 * fbox(npl) + B::W0T) * sizeof(double) + 32; }
 };
 
-// One thread per (slot0, chunk of y elements): ring over rows m1.  A chunk
-// starts P-1 elements early so its first rows are complete (redundant work
-// (P-1)/chunk); it writes rows m1 in [c·chunk, (c+1)·chunk) (+ the trailing
-// P-1 rows for the last chunk).
-template <int P, int Q>
-__global__ void __launch_bounds__(128) asm2_stage2(const Asm2bArgs a) {
-  constexpr int W = 2 * P - 1;
+template <int P, int Q, int T>
+__global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __grid_constant__ CUtensorMap fmap,
+                                                     int nplanes) {
+  using C = A3Cfg<P, Q, T>;
+  using C2 = A2Cfg<P, Q, T>;
+  constexpr int PT = C::PT, PTP = C::PTP, XR = C::XR, XK = C::XK, SP = C::SP, W = C::W, SR = C::SR;
+  constexpr int KL = max_ksteps<P, Q, T>(PTP / 8, XK / 4);
+  constexpr int NYB = A2_YS / 8, NST = PTP / 8;
+  extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t s0 = gid % a.NS0, c = gid / a.NS0;
-  const int K1 = a.tab.K[1];
-  const int nch = (K1 + a.chunk - 1) / a.chunk;
-  if (c >= nch) return;
-  const int64_t N0 = a.tab.N[0], N1 = a.tab.N[1];
-  const int64_t m0 = s0 / W, n0 = m0 + (s0 % W) - (P - 1);
-  if (m0 >= N0 || n0 < 0 || n0 >= N0) return;
-  const int64_t rp0 = a.pat.rp[0][m0], w0 = a.pat.rp[0][m0 + 1] - rp0;
-  const int64_t P0 = a.pat.rp[0][N0];
-  const int64_t r0 = n0 - a.pat.cl[0][rp0];
-  const int e_first = (int)c * a.chunk, e_last = min(K1, (int)(c + 1) * a.chunk);
-  const int e_start = max(0, e_first - (P - 1));
-  double ring[P][W];
-#pragma unroll
-  for (int r = 0; r < P; ++r)
-#pragma unroll
-    for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
-  auto flush = [&](int64_t m1, double* row) {
-    if (m1 < e_first || m1 >= N1) return;
-    if (m1 >= e_last && e_last != K1) return;
-    const int64_t m = m0 + N0 * m1;
-    if (m < a.row_lo || m >= a.row_hi) return;
-    const int64_t rp1 = a.pat.rp[1][m1], lo1 = a.pat.cl[1][rp1];
-    const int64_t start = rp0 * (a.pat.rp[1][m1 + 1] - rp1) + P0 * rp1 - *a.base;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      const int64_t n1 = m1 + k - (P - 1);
-      if (n1 >= 0 && n1 < N1) a.values[start + (n1 - lo1) * w0 + r0] = row[k];
+  const size_t fb = C2::fbox(nplanes);
+  double* Fs = sm;                 // [2][nplanes][A2_YS][XR]
+  double* W0 = Fs + 2 * fb;        // [4][XK][SP]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(W0 + C::W0T);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, m4 = lane & 3;
+  const int a0 = (blockIdx.x % a.nt0) * T;
+  const int xb0 = (a0 - (P - 1)) * Q;
+  const int64_t X1 = a.tab.X[1];
+  const int64_t y_lo = (int64_t)(blockIdx.x / a.nt0) * a.yc;
+  const int64_t y_hi = min64(X1, y_lo + a.yc);
+  const int nstage = (int)((y_hi - y_lo + A2_YS - 1) / A2_YS);
+  const unsigned fbytes = (unsigned)((size_t)nplanes * A2_YS * XR * sizeof(double));
+  for (int b = 0; b < 2; ++b)
+    for (size_t i = (size_t)nplanes * A2_YS * XR + tid; i < fb; i += A2_NT) Fs[b * fb + i] = 0.0;
+  if (tid < 2) dev::mbar_init(bar + tid, 1);
+  dev::fence_mbar_init();
+  dev::fence_proxy_async();
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < 2 && i < nstage; ++i) {
+      dev::mbar_expect_tx(bar + i, fbytes);
+      dev::tma_load_4d(Fs + i * fb, &fmap, bar + i, xb0, (int)(y_lo + i * A2_YS), 0, 0);
     }
-  };
-  for (int eb = e_start; eb < e_last; eb += P) {
+  fill_band_table<P, Q, T, false>(W0, a.tab, 0, a0, xb0);
+  __syncthreads();
+  for (int i = 0; i < nstage; ++i) {
+    const int buf = i & 1;
+    dev::mbar_wait(bar + buf, (unsigned)((i >> 1) & 1));
+    const double* Fb0 = Fs + buf * fb;
+    const int64_t y0 = y_lo + (int64_t)i * A2_YS;
+    for (int t = warp; t < NYB * NST; t += A2_NW) {
+      const int yb = t / NST, st = t % NST;
+      int k_lo, k_hi;
+      slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
+      const double* Fy = Fb0 + (yb * 8 + g8) * XR + m4 + k_lo * 4;
+      const double* Wk = W0 + (m4 + k_lo * 4) * SP + st * 8 + g8;
+      const int64_t y = y0 + yb * 8 + g8;
+      const int s = st * 8 + 2 * m4;
+      const int64_t gs0 = (int64_t)(a0 + s / SR) * W + s % SR;
+      const int64_t gs0b = (int64_t)(a0 + (s + 1) / SR) * W + (s + 1) % SR;
+      const bool ok0 = y < y_hi && s < PT && s % SR < W && gs0 < a.NS0;
+      const bool ok1 = y < y_hi && s + 1 < PT && (s + 1) % SR < W && gs0b < a.NS0;
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-    for (int r = 0; r < P; ++r) {
-      const int e1 = eb + r;
-      if (e1 >= e_last) break;
-      const int rr = (e1 - e_start) % P;  // == r (eb steps by P from e_start)
-      for (int q = 0; q < Q; ++q) {
-        const int64_t y = (int64_t)e1 * Q + q;
-        const double w = a.tab.wts[1][y];
-        double bv[2][P];
+      for (int b = 0; b < kMaxBlocks; ++b) {
+        if (b >= pl.nb) break;
+        const double* Fb = Fy + pl.b_plane[b] * (A2_YS * XR);
+        const double* Wb = Wk + pl.b_v0[b] * (XK * SP);
 #pragma unroll
-        for (int j = 0; j < P; ++j) {
-          bv[0][j] = a.tab.vals[1][((int64_t)0 * P + j) * a.tab.X[1] + y];
-          bv[1][j] = a.tab.md[1] >= 1 ? a.tab.vals[1][((int64_t)1 * P + j) * a.tab.X[1] + y] : 0.0;
-        }
-        for (int g = 0; g < pl.ng; ++g) {
-          const double hv = __ldg(a.G + (y * pl.ng + g) * a.NS0 + s0);
-          const int v = pl.g_v1[g];
-#pragma unroll
-          for (int jm = 0; jm < P; ++jm)
-#pragma unroll
-            for (int jn = 0; jn < P; ++jn) {
-              double wt = (w * bv[v & 1][jn]) * bv[v >> 1][jm];
-              ring[(r + jm) % P][jn - jm + P - 1] = fma(wt, hv, ring[(r + jm) % P][jn - jm + P - 1]);
-            }
+        for (int kk = 0; kk < KL; ++kk)
+          if (k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
+        if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
+          double* dst = a.G + (y * pl.ng + pl.b_g[b]) * a.NS0;
+          if (ok0) dst[gs0] = d0;
+          if (ok1) dst[gs0b] = d1;
+          d0 = d1 = 0.0;
         }
       }
-      (void)rr;
-      flush(e1, ring[r % P]);
-#pragma unroll
-      for (int k = 0; k < W; ++k) ring[r % P][k] = 0.0;
     }
-  }
-  // trailing rows of the last chunk: m1 in [K1, K1 + P - 1)
-  if (e_last == K1) {
-#pragma unroll
-    for (int t = 1; t < P; ++t) {
-      const int64_t m1 = K1 - 1 + t;
-      const int slot = (int)((m1 - e_start) % P);
-#pragma unroll
-      for (int s = 0; s < P; ++s)
-        if (s == slot) flush(m1, ring[s]);
+    __syncthreads();
+    if (tid == 0 && i + 2 < nstage) {
+      dev::fence_proxy_async();
+      dev::mbar_expect_tx(bar + buf, fbytes);
+      dev::tma_load_4d(Fs + buf * fb, &fmap, bar + buf, xb0, (int)(y0 + 2 * A2_YS), 0, 0);
     }
   }
 }
@@ -724,6 +713,27 @@ int asm3_tile_for(int P, const AsmPlan& pl, int nplanes) {
     case 4: return asm3_tile<4>(pl, nplanes);
     case 5: return asm3_tile<5>(pl, nplanes);
     case 6: return asm3_tile<6>(pl, nplanes);
+    default: return 0;
+  }
+}
+
+// row tile of the 2D stage-1 kernel: the largest of 8, 4, 2, 1 that fits
+template <int P>
+int asm2_tile(int nplanes) {
+  if (A2Cfg<P, P, 8>::smem(nplanes) <= 232448) return 8;
+  if (A2Cfg<P, P, 4>::smem(nplanes) <= 232448) return 4;
+  if (A2Cfg<P, P, 2>::smem(nplanes) <= 232448) return 2;
+  if (A2Cfg<P, P, 1>::smem(nplanes) <= 232448) return 1;
+  return 0;
+}
+
+int asm2_tile_for(int P, int nplanes) {
+  switch (P) {
+    case 2: return asm2_tile<2>(nplanes);
+    case 3: return asm2_tile<3>(nplanes);
+    case 4: return asm2_tile<4>(nplanes);
+    case 5: return asm2_tile<5>(nplanes);
+    case 6: return asm2_tile<6>(nplanes);
     default: return 0;
   }
 }
@@ -764,11 +774,10 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
         if (s.plan.b_v0[b] != 0) return false;
     }
   if (s.fs.p < 2 || s.fs.p > 6 || s.fs.k != s.fs.p) return false;
-  if (d == 3) {
-    if (asm3_tile_for(s.fs.p, s.plan, p->n_planes) == 0) return false;  // stage-1/2 tile must fit
-    // TMA: 16-byte aligned rows and plane stride
-    if ((s.fs.npt[0] * 8) % 16 != 0 || (p->plane_stride * 8) % 16 != 0 || p->n_planes > 256) return false;
-  }
+  if (d == 3 && asm3_tile_for(s.fs.p, s.plan, p->n_planes) == 0) return false;  // stage-1/2 tile must fit
+  if (d == 2 && asm2_tile_for(s.fs.p, p->n_planes) == 0) return false;
+  // TMA: 16-byte aligned rows and plane stride
+  if ((s.fs.npt[0] * 8) % 16 != 0 || (p->plane_stride * 8) % 16 != 0 || p->n_planes > 256) return false;
   (void)D;
   if (out) *out = s;
   return true;
@@ -793,7 +802,8 @@ size_t asm_workspace(const AsmShape& s) {
     return (size_t)s.zpts * s.plan.nh * (s.fs.nfn[1] * W) * (s.fs.nfn[0] * W) * sizeof(double) +
            (size_t)s.fs.nel[2] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
   }
-  return (size_t)s.fs.npt[1] * s.plan.ng * (s.fs.nfn[0] * W) * sizeof(double) + 512;
+  return (size_t)s.fs.npt[1] * s.plan.ng * (s.fs.nfn[0] * W) * sizeof(double) +
+         (size_t)s.fs.nel[1] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
 }
 
 // z elements the row range needs (rows of DoF layers [m2a, m2b] are summed
@@ -893,18 +903,53 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.w2g = w2g;
   b.e_lo = z.e_lo;
   b.e_hi = z.e_hi;
+  b.chunk = z.e_hi - z.e_lo;
+  b.ngrp = s.plan.nh;
+  for (int h = 0; h < 4; ++h) b.grp_v[h] = h < s.plan.nh ? s.plan.h_v2[h] : 0;
   {
     const int64_t n = (int64_t)tab.K[2] * Q * P * P * 4;
-    asm3_w2_kernel<P, Q><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);
-    IGS_LAUNCH_CHECK("asm3_w2_kernel");
+    asm_wlast_kernel<P, Q, 3><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);
+    IGS_LAUNCH_CHECK("asm_wlast_kernel");
   }
   int64_t threads = a.NS0 * a.NS1;
   constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
-  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_stage3<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem3),
                      "smem attribute"));
-  asm3_stage3<P, Q><<<(unsigned)ceil_div(threads, NT3), NT3, smem3, st>>>(b);
-  IGS_LAUNCH_CHECK("asm3_stage3");
+  asm_sweep<P, Q, 3><<<(unsigned)ceil_div(threads, NT3), NT3, smem3, st>>>(b);
+  IGS_LAUNCH_CHECK("asm_sweep<3>");
+  return IGS_OK;
+}
+
+template <int P, int Q, int T>
+igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double* planes, double* G,
+                          cudaStream_t st) {
+  using C = A3Cfg<P, Q, T>;
+  Asm2Args a{};
+  a.plan = s.plan;
+  a.tab = tab_args(p);
+  a.G = G;
+  a.NS0 = s.fs.nfn[0] * C::W;
+  a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
+  const size_t smem = A2Cfg<P, Q, T>::smem(p->n_planes);
+  if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
+  CUtensorMap fmap;
+  {
+    const int64_t dims[4] = {s.fs.npt[0], s.fs.npt[1], 1, p->n_planes};
+    const unsigned box[4] = {(unsigned)C::XR, (unsigned)A2_YS, 1u, (unsigned)p->n_planes};
+    IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
+  }
+  // y chunks: ~4 CTAs per SM in total, whole TMA boxes
+  const int64_t want = ceil_div(148 * 4, a.nt0);
+  int64_t yc = ceil_div(s.fs.npt[1], want > 0 ? want : 1);
+  yc = ceil_div(yc, A2_YS) * A2_YS;
+  a.yc = (int)yc;
+  const int64_t nyc = ceil_div(s.fs.npt[1], yc);
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm2_stage1<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem),
+                     "smem attribute"));
+  asm2_stage1<P, Q, T><<<(unsigned)(a.nt0 * nyc), A2_NT, smem, st>>>(a, fmap, p->n_planes);
+  IGS_LAUNCH_CHECK("asm2_stage1");
   return IGS_OK;
 }
 
@@ -912,38 +957,54 @@ template <int P, int Q>
 igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
                    const int64_t* base, const double* planes, double* values, double* G, cudaStream_t st) {
   constexpr int W = 2 * P - 1;
-  Asm2Args a{};
-  a.plan = s.plan;
-  a.tab = tab_args(p);
-  a.planes = planes;
-  a.pstride = p->plane_stride;
-  a.G = G;
-  a.NS0 = s.fs.nfn[0] * W;
-  int64_t total = a.NS0 * s.fs.npt[1];
-  int64_t grid = ceil_div(total, 256);
-  if (grid > 148 * 32) grid = 148 * 32;
-  asm2_stage1<P, Q><<<(unsigned)grid, 256, 0, st>>>(a);
-  IGS_LAUNCH_CHECK("asm2_stage1");
-  Asm2bArgs b{};
+  switch (asm2_tile<P>(p->n_planes)) {
+    case 8: IGS_TRY((launch2_stage1<P, Q, 8>(p, s, planes, G, st))); break;
+    case 4: IGS_TRY((launch2_stage1<P, Q, 4>(p, s, planes, G, st))); break;
+    case 2: IGS_TRY((launch2_stage1<P, Q, 2>(p, s, planes, G, st))); break;
+    case 1: IGS_TRY((launch2_stage1<P, Q, 1>(p, s, planes, G, st))); break;
+    default: return fail(IGS_ECAPACITY, "2D assembly tile does not fit shared memory");
+  }
+  struct {
+    int64_t NS0;
+  } a{s.fs.nfn[0] * W};
+  const TabArgs tab = tab_args(p);
+  Asm3bArgs b{};
   b.plan = s.plan;
-  b.tab = a.tab;
-  b.G = G;
+  b.tab = tab;
+  b.H = G;
   b.NS0 = a.NS0;
-  // enough (slot, chunk) threads to fill the GPU, chunks >= 4(P-1) elements
-  int K1 = (int)s.fs.nel[1];
-  int want = (int)ceil_div(148 * 1024, a.NS0);
-  int chunk = (int)ceil_div(K1, want > 0 ? want : 1);
-  if (chunk < 4 * (P - 1)) chunk = 4 * (P - 1);
-  if (chunk > K1) chunk = K1;
-  b.chunk = chunk;
+  b.NS1 = 1;
   b.pat = pat;
   b.row_lo = row_lo;
   b.row_hi = row_hi;
   b.base = base;
   b.values = values;
-  int64_t threads = a.NS0 * ceil_div(K1, chunk);
-  asm2_stage2<P, Q><<<(unsigned)ceil_div(threads, 128), 128, 0, st>>>(b);
-  IGS_LAUNCH_CHECK("asm2_stage2");
+  const int K1 = (int)s.fs.nel[1];
+  double* wlg = G + (size_t)s.fs.npt[1] * s.plan.ng * a.NS0;
+  b.w2g = wlg;
+  b.e_lo = 0;
+  b.e_hi = K1;
+  // enough (slot, chunk) threads to fill the GPU, chunks >= 2(P-1) elements
+  int want = (int)ceil_div(148 * 1024, a.NS0);
+  int chunk = (int)ceil_div(K1, want > 0 ? want : 1);
+  if (chunk < 2 * (P - 1)) chunk = 2 * (P - 1);
+  if (chunk > K1) chunk = K1;
+  b.chunk = chunk;
+  if (s.plan.ng > 4) return fail(IGS_ECAPACITY, "2D fused assembly sums at most 4 variant groups");
+  b.ngrp = s.plan.ng;
+  for (int g = 0; g < 4; ++g) b.grp_v[g] = g < s.plan.ng ? s.plan.g_v1[g] : 0;
+  {
+    const int64_t n = (int64_t)K1 * Q * P * P * 4;
+    asm_wlast_kernel<P, Q, 2><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, wlg);
+    IGS_LAUNCH_CHECK("asm_wlast_kernel");
+  }
+  const int64_t threads = a.NS0 * ceil_div(K1, chunk);
+  constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem3),
+                     "smem attribute"));
+  asm_sweep<P, Q, 2><<<(unsigned)ceil_div(threads, NT3), NT3, smem3, st>>>(b);
+  IGS_LAUNCH_CHECK("asm_sweep<2>");
   return IGS_OK;
 }
 
