@@ -146,14 +146,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// TMA: one 4D box (points of one element, 8 lines, 1 point layer, all planes).
-// L2 prefetch of one TMA box (no shared memory, no barrier): keeps HBM busy
-// while the CTA is in its shared-memory-only phases.
-__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map),
-               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
+// TMA: one 4D box (points of EPB elements, 8 lines, 1 point layer, all planes).
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
   asm volatile(
@@ -166,7 +159,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 // Tile geometry and shared-memory plan.  Q2B point layers of z are processed
 // per batch; warp w owns (point layer w / NLG of the batch, line group
 // w % NLG) in the X phase and sweeps all EX elements of its 8 lines.
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_, int EPB_ = 1>
 struct Cfg {
   static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
   static_assert(Q % Q2B == 0, "batches tile the element's point layers");
@@ -190,8 +183,11 @@ struct Cfg {
   static constexpr int NA = STIFF ? 2 : 1;     // z variants: value, z-derivative
   static constexpr int NV = STIFF ? 3 : 1;     // (y, z) variants: 00, 10, 01
   static constexpr int NPL = (MASS ? 1 : 0) + (STIFF ? 6 : 0);  // coefficient planes
-  static constexpr int QE = (Q + 1) & ~1;      // TMA box width (16-byte multiple)
-  static constexpr int STG = STG_;             // TMA stages per warp
+  static constexpr int EPB = EPB_;             // elements per TMA box
+  static_assert(EX % EPB == 0, "boxes tile the element row");
+  static constexpr int NBX = EX / EPB;         // boxes per (batch, line group)
+  static constexpr int QE = (EPB * Q + 1) & ~1;  // TMA box width (16-byte multiple)
+  static constexpr int STG = STG_;             // TMA stages (boxes) per warp
   static constexpr int FST = NPL * 8 * QE;     // doubles per stage
   static constexpr int LXR = FYP * RP;         // one [n1][n0] plane
   static constexpr int XR = P * LXR;           // x ring (P DoF layers)
@@ -207,12 +203,11 @@ struct Cfg {
   static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the tile allows
 };
 
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_>
-__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
-                                  Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::MINB)
-    apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap,
-                   const __grid_constant__ CUtensorMap fmap_row) {
-  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>;
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_, int EPB_>
+__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_>::NT,
+                                  Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_>::MINB)
+    apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap) {
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_>;
   constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY;
   constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR, STG = C::STG, FST = C::FST, QE = C::QE;
   constexpr int NLG = C::NLG, NB = C::NB, CQL = C::CQL, NA = C::NA, NV = C::NV;
@@ -250,30 +245,24 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // layer (batch·Q2B + w/NLG) and line group w%NLG, element by element; each
   // (batch, element) is one TMA box, STG boxes in flight per warp.
   const int wq = warp / NLG, wlg = warp % NLG;
-  // ring stage / parity of a task: static per element when STG divides EX
-  // into an even number of rounds, otherwise from the running task index
-  constexpr bool kStaticRing = EX % STG == 0 && (EX / STG) % 2 == 0;
+  // ring stage / parity of a task: static per box when STG divides the
+  // boxes of a row into an even number of rounds, else from the task index
+  constexpr int EPB = C::EPB, NBX = C::NBX;
+  constexpr bool kStaticRing = NBX % STG == 0 && (NBX / STG) % 2 == 0;
   // every element of the tile interior (e in [P-1, K0-P]): one shared table
   const bool tile_uniform = a.uni_x && ex0 >= P - 1 && ex0 + EX - 1 <= a.K0 - P;
-  const int ntask = (z1 - z0) * NB * EX;
+  const int ntask = (z1 - z0) * NB * NBX;
   uint64_t* mybar = bars + warp * STG;
   double* mystage = Fs + warp * STG * FST;
-  auto issue = [&](int idx) {  // one lane
-    const int batch = idx / EX, ex = idx % EX;
+  auto issue = [&](int idx) {  // one lane: box idx = (batch, EPB elements)
+    const int batch = idx / NBX, bx = idx % NBX;
     const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
     uint64_t* bar = mybar + idx % STG;
     mbar_expect_tx(bar, (unsigned)(FST * sizeof(double)));
     if (a.l2pf < 0)
       tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, ex0 * Q, ey0 * Q + wlg * 8, 0, 0);
     else
-      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + ex) * Q, ey0 * Q + wlg * 8, zq, 0);
-  };
-  // L2 prefetch of this warp's whole 8-line x row of task batch `batch`
-  // (one box of TX points: long contiguous DRAM bursts)
-  auto prefetch_batch = [&](int batch) {
-    if (batch * EX >= ntask) return;
-    const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
-    tma_prefetch_4d(&fmap_row, ex0 * Q, ey0 * Q + wlg * 8, zq, 0);
+      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + bx * EPB) * Q, ey0 * Q + wlg * 8, zq, 0);
   };
   // lanes past the box width of odd Q read neighbouring stage memory (masked
   // by zero weights): keep it finite
@@ -478,7 +467,8 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         PHASE_MARK(2);  // Y
         const bool line_ok = (ey0 + line / Q) < a.K1;
         const double wyz = Wz[q2] * Wy[line];
-        const int widx0 = widx;         // = batch·EX
+        const int widx0 = widx;         // = batch·NBX
+        int stage = 0;                  // ring stage of the current box
         // running X^T window over columns [ex, ex+8): lane m holds ex+2m, ex+2m+1
         double w00[2] = {0.0, 0.0}, w10[2] = {0.0, 0.0}, w01[2] = {0.0, 0.0};
         // table fragments: forward B^T[j][q = n] (D column n is point n, so a
@@ -525,14 +515,17 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 #ifdef IGS_PHASE_TIMING
           long long tw0_ = clock64();
 #endif
-          const int gi = kStaticRing ? ex : widx0 + ex;
-          const int stage = gi % STG;
-          mbar_wait(mybar + stage, (unsigned)((gi / STG) & 1));
+          const int bx = ex / EPB, eo = ex % EPB;
+          if (eo == 0) {
+            const int gi = kStaticRing ? bx : widx0 + bx;
+            stage = gi % STG;
+            mbar_wait(mybar + stage, (unsigned)((gi / STG) & 1));
+          }
 #ifdef IGS_PHASE_TIMING
           if (tid == 0) atomicAdd(&g_phase_cycles[5], (unsigned long long)(clock64() - tw0_));
 #endif
           // [plane][line][q]: the lane's points 2m, 2m+1 as one 16-byte load
-          const double* F = mystage + stage * FST + g * QE + 2 * m;
+          const double* F = mystage + stage * FST + g * QE + eo * Q + 2 * m;
           double fv[7][2];
           auto ld2 = [&](int pl, double* o) {
             const double2 v = *reinterpret_cast<const double2*>(F + pl * 8 * QE);
@@ -588,8 +581,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           }
           // every lane's reads of this stage have been consumed (the MMAs above
           // depend on them): hand the stage to the next box of this warp
-          __syncwarp();
-          if (lane == 0 && widx0 + ex + STG < ntask) issue(widx0 + ex + STG);
+          if (eo == EPB - 1) {
+            __syncwarp();
+            if (lane == 0 && widx0 + bx + STG < ntask) issue(widx0 + bx + STG);
+          }
           // column ex is complete (no later element touches it): store it over
           // C's column ex, which no later element reads, then slide the window.
           __syncwarp();
@@ -618,7 +613,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) cf[v][s2] = cn[v][s2];
         }
-        widx = widx0 + EX;
+        widx = widx0 + NBX;
         // remaining columns [EX, EX + 8): lane m holds EX + 2m + c
         __syncwarp();
 #pragma unroll
@@ -743,13 +738,13 @@ __global__ void apply_reduce_kernel(const ReduceArgs r) {
 struct Launch {
   int EX, EY, NT, NPL, QE;
   size_t smem;
-  void (*kernel)(ApplyArgs, CUtensorMap, CUtensorMap);
+  void (*kernel)(ApplyArgs, CUtensorMap);
 };
 
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2, int EPB = 1>
 Launch make_launch() {
-  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG>;
-  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG>};
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>;
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>};
 }
 
 // Development switch (IGS_APPLY_VARIANT) for comparing tile shapes on the box.
@@ -773,8 +768,10 @@ bool pick(int P, int Q, Launch* L) {
     case 4: *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>(); return true;
     case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
     case 6:
-      if (apply_variant() == 1) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
-      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
+      // 2-element boxes (96-byte rows: whole sectors, half the TMA issues);
+      // 7 planes do not fit them, single-element boxes in a 3-stage ring
+      if (apply_variant() == 1 || (MASS && STIFF)) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
+      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2, 2>();
       return true;
     case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
     case 8:
@@ -904,13 +901,12 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
   a.ntx = t.ntx; a.nty = t.nty; a.nch = t.nch; a.ez = t.ez;
   a.scratch = reinterpret_cast<double*>(ws);
   a.box = t.box;
-  CUtensorMap fmap, fmap_row;
+  CUtensorMap fmap;
   IGS_TRY(coeff_tensor_map(&fmap, planes, p->plane_stride, D, L, (unsigned)L.QE));
-  IGS_TRY(coeff_tensor_map(&fmap_row, planes, p->plane_stride, D, L, (unsigned)(L.EX * L.QE)));
   IGS_TRY(cuda_check(cudaFuncSetAttribute(L.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)L.smem), "smem attribute"));
   unsigned grid = (unsigned)(t.ntx * t.nty * t.nch);
-  L.kernel<<<grid, L.NT, L.smem, st>>>(a, fmap, fmap_row);
+  L.kernel<<<grid, L.NT, L.smem, st>>>(a, fmap);
   IGS_LAUNCH_CHECK("apply3d_kernel");
   if (flags & IGS_FLAG_KERNEL_ONLY) return IGS_OK;
   ReduceArgs r{};
