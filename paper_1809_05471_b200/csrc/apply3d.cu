@@ -736,7 +736,7 @@ __global__ void apply_reduce_kernel(const ReduceArgs r) {
 // ---- instantiation table ----------------------------------------------------
 
 struct Launch {
-  int EX, EY, NT, NPL, QE;
+  int EX, EY, NT, NPL, QE, EPB;
   size_t smem;
   void (*kernel)(ApplyArgs, CUtensorMap);
 };
@@ -744,7 +744,7 @@ struct Launch {
 template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2, int EPB = 1>
 Launch make_launch() {
   using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>;
-  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>};
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, EPB, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>};
 }
 
 // Development switch (IGS_APPLY_VARIANT) for comparing tile shapes on the box.
@@ -818,6 +818,14 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
   return t;
 }
 
+// L2 promotion of the coefficient boxes: 64-byte box rows (one element of
+// 8 points) gain from 256-byte promotion (the warp's next elements arrive
+// with them: C5 -3 %); wider rows take whole sectors without promotion
+// (C4: DRAM reads = B_alg exactly instead of +3.6 %, same time).
+CUtensorMapL2promotion l2_promotion(const Launch& L) {
+  return L.EPB > 1 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // The coefficient planes as one 4D tensor (x, y, z points, plane) for TMA.
 // cuTensorMapEncodeTiled comes from the driver through the runtime's entry
 // point query, so the library does not link libcuda directly.
@@ -838,7 +846,7 @@ igs_status coeff_tensor_map(CUtensorMap* map, const double* planes, int64_t pstr
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(planes), dims, strides,
                       boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      l2_promotion(L), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(IGS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return IGS_OK;
 }
