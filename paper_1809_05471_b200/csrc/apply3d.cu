@@ -146,7 +146,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// TMA: one 4D box (points of EPB elements, 8 lines, 1 point layer, all planes).
+// TMA: one 4D box (8 points, 8 lines, 1 point layer, all planes).
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {
   asm volatile(
@@ -159,7 +159,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 // Tile geometry and shared-memory plan.  Q2B point layers of z are processed
 // per batch; warp w owns (point layer w / NLG of the batch, line group
 // w % NLG) in the X phase and sweeps all EX elements of its 8 lines.
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_, int EPB_ = 1>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_>
 struct Cfg {
   static_assert(P >= 2 && P <= 8 && Q >= 1 && Q <= 8, "orders 2..8, up to 8 points per element");
   static_assert(Q % Q2B == 0, "batches tile the element's point layers");
@@ -183,10 +183,16 @@ struct Cfg {
   static constexpr int NA = STIFF ? 2 : 1;     // z variants: value, z-derivative
   static constexpr int NV = STIFF ? 3 : 1;     // (y, z) variants: 00, 10, 01
   static constexpr int NPL = (MASS ? 1 : 0) + (STIFF ? 6 : 0);  // coefficient planes
-  static constexpr int EPB = EPB_;             // elements per TMA box
-  static_assert(EX % EPB == 0, "boxes tile the element row");
-  static constexpr int NBX = EX / EPB;         // boxes per (batch, line group)
-  static constexpr int QE = (EPB * Q + 1) & ~1;  // TMA box width (16-byte multiple)
+  // The X sweep walks 8-point windows of the tile's TX = EX·Q points (one
+  // MMA n-tile each, whatever Q is); window w spans elements
+  // [8w/Q, (8w+7)/Q] and DoF columns [c0(w), c0(w) + 8), c0(w) = 8w/Q.
+  static_assert((EX * Q) % 8 == 0, "windows tile the element row");
+  static constexpr int NWIN = EX * Q / 8;      // windows per (batch, line group)
+  static constexpr int NBX = NWIN;             // TMA boxes (one window each)
+  static constexpr int QE = 8;                 // TMA box width (64-byte rows)
+  static constexpr int c0w(int w) { return (8 * w) / Q; }
+  static constexpr int gcd8(int q) { return q % 8 == 0 ? 8 : q % 4 == 0 ? 4 : q % 2 == 0 ? 2 : 1; }
+  static constexpr int PER = Q / gcd8(Q);      // windows per period of the table pattern
   static constexpr int STG = STG_;             // TMA stages (boxes) per warp
   static constexpr int FST = NPL * 8 * QE;     // doubles per stage
   static constexpr int LXR = FYP * RP;         // one [n1][n0] plane
@@ -195,7 +201,7 @@ struct Cfg {
   static constexpr int CQL = TY * RP;          // one C/R variant plane
   static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
   static constexpr int YR = P * LXR;           // y ring
-  static constexpr int TBX = EX * 128, TBY = EY * 128, TBZ = 256;  // [e][v][q8][j8]; Tz double-buffered
+  static constexpr int TBX = NWIN * 128, TBY = EY * 128, TBZ = 256;  // Tw [w][v][c8][pt8]; Ty/Tz [e][v][q8][j8]
   static constexpr int WW = TX + TY + 16;
   static constexpr int FS = NW * STG * FST;    // coefficient staging
   static constexpr int TOTAL = FS + XR + AQ + CQ + YR + TBX + TBY + TBZ + WW;
@@ -203,11 +209,11 @@ struct Cfg {
   static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;  // CTAs per SM the tile allows
 };
 
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_, int EPB_>
-__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_>::NT,
-                                  Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_>::MINB)
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG_>
+__global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
+                                  Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::MINB)
     apply3d_kernel(const ApplyArgs a, const __grid_constant__ CUtensorMap fmap) {
-  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_>;
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>;
   constexpr int FX = C::FX, FY = C::FY, RP = C::RP, TX = C::TX, TY = C::TY;
   constexpr int NT = C::NT, NW = C::NW, LXR = C::LXR, STG = C::STG, FST = C::FST, QE = C::QE;
   constexpr int NLG = C::NLG, NB = C::NB, CQL = C::CQL, NA = C::NA, NV = C::NV;
@@ -218,8 +224,8 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
   // C, then R in place, then the warp's Y^T partials S_v over its own rows
   double* Cq = Aq + C::AQ;      // [Q2B][NV][TY][RP]
   double* Yr = Cq + C::CQ;      // [P][FYP][RP]
-  double* Tx = Yr + C::YR;      // [EX][2][8][8]
-  double* Ty = Tx + C::TBX;     // [EY][2][8][8]
+  double* Tw = Yr + C::YR;      // [NWIN][2][8 c][8 pt]  window tables
+  double* Ty = Tw + C::TBX;     // [EY][2][8][8]
   double* Tzb = Ty + C::TBY;    // [2 buffers][2][8][8]
   double* Wx = Tzb + C::TBZ;    // [TX]
   double* Wy = Wx + TX;         // [TY]
@@ -247,14 +253,14 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
   const int wq = warp / NLG, wlg = warp % NLG;
   // ring stage / parity of a task: static per box when STG divides the
   // boxes of a row into an even number of rounds, else from the task index
-  constexpr int EPB = C::EPB, NBX = C::NBX;
+  constexpr int NBX = C::NBX, NWIN = C::NWIN;
   constexpr bool kStaticRing = NBX % STG == 0 && (NBX / STG) % 2 == 0;
   // every element of the tile interior (e in [P-1, K0-P]): one shared table
   const bool tile_uniform = a.uni_x && ex0 >= P - 1 && ex0 + EX - 1 <= a.K0 - P;
   const int ntask = (z1 - z0) * NB * NBX;
   uint64_t* mybar = bars + warp * STG;
   double* mystage = Fs + warp * STG * FST;
-  auto issue = [&](int idx) {  // one lane: box idx = (batch, EPB elements)
+  auto issue = [&](int idx) {  // one lane: box idx = (batch, window)
     const int batch = idx / NBX, bx = idx % NBX;
     const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
     uint64_t* bar = mybar + idx % STG;
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
     if (a.l2pf < 0)
       tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, ex0 * Q, ey0 * Q + wlg * 8, 0, 0);
     else
-      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, (ex0 + bx * EPB) * Q, ey0 * Q + wlg * 8, zq, 0);
+      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, ex0 * Q + bx * 8, ey0 * Q + wlg * 8, zq, 0);
   };
   // lanes past the box width of odd Q read neighbouring stage memory (masked
   // by zero weights): keep it finite
@@ -277,11 +283,13 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
   // ---- prologue ---------------------------------------------------------------
   for (int i = tid; i < C::TOTAL - C::FS; i += NT) Xr[i] = 0.0;  // all MMA padding is zero
   __syncthreads();
-  for (int i = tid; i < EX * 2 * Q * P; i += NT) {
-    int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
-    int ge = ex0 + e;
-    if (ge < a.K0)
-      Tx[((e * 2 + v) * 8 + q) * 8 + j] = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ge * Q + q];
+  // Tw[w][v][c][pt] = B^v of DoF column c0(w) + c at window point pt (zero
+  // outside the support or past the mesh)
+  for (int i = tid; i < NWIN * 128; i += NT) {
+    const int pt = i % 8, c = (i / 8) % 8, v = (i / 64) % 2, w = i / 128;
+    const int el = (8 * w + pt) / Q, j = (8 * w) / Q + c - el, ge = ex0 + el;
+    if (ge < a.K0 && j >= 0 && j < P)
+      Tw[i] = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ex0 * Q + 8 * w + pt];
   }
   for (int i = tid; i < EY * 2 * Q * P; i += NT) {
     int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
@@ -469,29 +477,29 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
         const double wyz = Wz[q2] * Wy[line];
         const int widx0 = widx;         // = batch·NBX
         int stage = 0;                  // ring stage of the current box
-        // running X^T window over columns [ex, ex+8): lane m holds ex+2m, ex+2m+1
+        // running X^T window over DoF columns [c0(w), c0(w) + 8): lane m holds
+        // c0 + 2m, c0 + 2m + 1
         double w00[2] = {0.0, 0.0}, w10[2] = {0.0, 0.0}, w01[2] = {0.0, 0.0};
-        // table fragments: forward B^T[j][q = n] (D column n is point n, so a
-        // lane's two D values are the adjacent points 2m, 2m+1) and the
-        // transpose B[q][j] with the k-chunk s covering points q = 2m + s;
-        // hoisted when every element of the tile is interior
+        // window table fragments: forward B^T[c][pt = n] (D column n is window
+        // point n, so a lane's two D values are the adjacent points 2m, 2m+1)
+        // and the transpose B[pt][c] with k-chunk s covering points 2m + s;
+        // hoisted when the tile is interior and every window has one pattern
         double fb0[2], fb1[2], tb0[2], tb1[2];
-        auto load_tab = [&](int ex) {
-          const double* T0 = Tx + (ex * 2 + 0) * 64;
-          const double* T1 = Tx + (ex * 2 + 1) * 64;
+        auto load_tab = [&](int w) {
+          const double* T0 = Tw + (w * 2 + 0) * 64;
+          const double* T1 = Tw + (w * 2 + 1) * 64;
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
-            fb0[s] = T0[g * 8 + m + 4 * s];
-            fb1[s] = STIFF ? T1[g * 8 + m + 4 * s] : 0.0;
-            tb0[s] = T0[(2 * m + s) * 8 + g];
-            tb1[s] = STIFF ? T1[(2 * m + s) * 8 + g] : 0.0;
+            fb0[s] = T0[(m + 4 * s) * 8 + g];
+            fb1[s] = STIFF ? T1[(m + 4 * s) * 8 + g] : 0.0;
+            tb0[s] = T0[g * 8 + 2 * m + s];
+            tb1[s] = STIFF ? T1[g * 8 + 2 * m + s] : 0.0;
           }
         };
-        if (tile_uniform) load_tab(0);
-        // point validity masks (the lane's points q = 2m and 2m + 1)
-        const double msk0 = (2 * m < Q) ? 1.0 : 0.0, msk1 = (2 * m + 1 < Q) ? 1.0 : 0.0;
-        // software pipeline: C fragments of element ex+1 are loaded while ex
-        // computes (element ex only ever writes column ex, below them)
+        const bool hoist = tile_uniform && C::PER == 1;
+        if (hoist) load_tab(0);
+        // software pipeline: C fragments of window w+1 are loaded while w
+        // computes (window w only ever writes columns below c0(w+1))
         double cf[3][2], cn[3][2];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -499,33 +507,35 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
           cf[1][s] = STIFF ? Crow[CQL + m + 4 * s] : 0.0;
           cf[2][s] = STIFF ? Crow[2 * CQL + m + 4 * s] : 0.0;
         }
+        const double wl = line_ok ? wyz : 0.0;
 #pragma unroll
-        for (int ex = 0; ex < EX; ++ex) {
-          if (!tile_uniform) load_tab(ex);
-          if (ex + 1 < EX) {
+        for (int w = 0; w < NWIN; ++w) {
+          const int c0 = C::c0w(w);
+          if (!hoist) load_tab(w);
+          if (w + 1 < NWIN) {
+            const int c1 = C::c0w(w + 1);
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
-              cn[0][s] = Crow[ex + 1 + m + 4 * s];
-              cn[1][s] = STIFF ? Crow[CQL + ex + 1 + m + 4 * s] : 0.0;
-              cn[2][s] = STIFF ? Crow[2 * CQL + ex + 1 + m + 4 * s] : 0.0;
+              cn[0][s] = Crow[c1 + m + 4 * s];
+              cn[1][s] = STIFF ? Crow[CQL + c1 + m + 4 * s] : 0.0;
+              cn[2][s] = STIFF ? Crow[2 * CQL + c1 + m + 4 * s] : 0.0;
             }
           }
-          // coefficients of (element ex, these 8 lines, point layer q2): wait
+          // coefficients of (window w, these 8 lines, point layer q2): wait
           // for the TMA box first so its shared-memory reads overlap the MMAs
 #ifdef IGS_PHASE_TIMING
           long long tw0_ = clock64();
 #endif
-          const int bx = ex / EPB, eo = ex % EPB;
-          if (eo == 0) {
-            const int gi = kStaticRing ? bx : widx0 + bx;
+          {
+            const int gi = kStaticRing ? w : widx0 + w;
             stage = gi % STG;
             mbar_wait(mybar + stage, (unsigned)((gi / STG) & 1));
           }
 #ifdef IGS_PHASE_TIMING
           if (tid == 0) atomicAdd(&g_phase_cycles[5], (unsigned long long)(clock64() - tw0_));
 #endif
-          // [plane][line][q]: the lane's points 2m, 2m+1 as one 16-byte load
-          const double* F = mystage + stage * FST + g * QE + eo * Q + 2 * m;
+          // [plane][line][pt]: the lane's points 2m, 2m+1 as one 16-byte load
+          const double* F = mystage + stage * FST + g * QE + 2 * m;
           double fv[7][2];
           auto ld2 = [&](int pl, double* o) {
             const double2 v = *reinterpret_cast<const double2*>(F + pl * 8 * QE);
@@ -541,9 +551,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
             ld2(p02, fv[5]);
             ld2(p12, fv[6]);
           }
-          // forward: U^T[line][q] = Σ_j C^T[line][j] · B^T[j][q].  A lane's two
-          // D values (points 2m, 2m+1) are its A-fragment columns of the two
-          // k-chunks of the transposed product below (no shuffles).
+          // forward: U^T[line][pt] = Σ_c C^T[line][c0 + c] · B^T[c][pt].  A
+          // lane's two D values (points 2m, 2m+1) are its A-fragment columns
+          // of the two k-chunks of the transposed product below (no shuffles).
           double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
@@ -554,22 +564,21 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
               dmma(uz[0], uz[1], cf[2][s], fb0[s]);
             }
           }
-          const double rowm = ((ex0 + ex) < a.K0 && line_ok) ? wyz : 0.0;
+          // pointwise (the x weight is zero past the mesh)
           double g0[2], gx[2], gy[2], gz[2];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const int q = 2 * m + c;
-            const double w = rowm * (c == 0 ? msk0 : msk1) * Wx[(ex * Q + q) < TX ? ex * Q + q : 0];
-            if (MASS) g0[c] = w * (fv[0][c] * u[c]);
+            const double wt = wl * Wx[8 * w + 2 * m + c];
+            if (MASS) g0[c] = wt * (fv[0][c] * u[c]);
             if (STIFF) {
               const double f00 = fv[1][c], f11 = fv[2][c], f22 = fv[3][c];
               const double f01 = fv[4][c], f02 = fv[5][c], f12 = fv[6][c];
-              gx[c] = w * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
-              gy[c] = w * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
-              gz[c] = w * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
+              gx[c] = wt * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
+              gy[c] = wt * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
+              gz[c] = wt * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
             }
           }
-          // transpose into the window: W^T[line][j] += Σ_q g^T[line][q] · B[q][j]
+          // transpose into the window: W^T[line][c] += Σ_pt g^T[line][pt] · B[pt][c]
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             if (MASS) dmma(w00[0], w00[1], g0[s], tb0[s]);
@@ -581,44 +590,54 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_, EPB_
           }
           // every lane's reads of this stage have been consumed (the MMAs above
           // depend on them): hand the stage to the next box of this warp
-          if (eo == EPB - 1) {
-            __syncwarp();
-            if (lane == 0 && widx0 + bx + STG < ntask) issue(widx0 + bx + STG);
-          }
-          // column ex is complete (no later element touches it): store it over
-          // C's column ex, which no later element reads, then slide the window.
           __syncwarp();
-          if (m == 0) {
-            Crow[ex] = w00[0];
-            if (STIFF) {
-              Crow[CQL + ex] = w10[0];
-              Crow[2 * CQL + ex] = w01[0];
-            }
-          }
-          {
-            double nx = __shfl_down_sync(0xffffffffu, w00[0], 1, 4);
-            w00[0] = w00[1];
-            w00[1] = (m == 3) ? 0.0 : nx;
-            if (STIFF) {
-              nx = __shfl_down_sync(0xffffffffu, w10[0], 1, 4);
-              w10[0] = w10[1];
-              w10[1] = (m == 3) ? 0.0 : nx;
-              nx = __shfl_down_sync(0xffffffffu, w01[0], 1, 4);
-              w01[0] = w01[1];
-              w01[1] = (m == 3) ? 0.0 : nx;
-            }
-          }
+          if (lane == 0 && widx0 + w + STG < ntask) issue(widx0 + w + STG);
+          // columns [c0, c0 + d) are complete (no later window touches them):
+          // store them over C's columns, which no later window reads, then
+          // slide the accumulator window by d columns.
+          const int d = (w + 1 < NWIN ? C::c0w(w + 1) : c0 + 8) - c0;
+          if (w + 1 < NWIN) {
+            __syncwarp();
 #pragma unroll
-          for (int v = 0; v < 3; ++v)
+            for (int c = 0; c < 2; ++c)
+              if (2 * m + c < d) {
+                Crow[c0 + 2 * m + c] = w00[c];
+                if (STIFF) {
+                  Crow[CQL + c0 + 2 * m + c] = w10[c];
+                  Crow[2 * CQL + c0 + 2 * m + c] = w01[c];
+                }
+              }
+            // new column 2m + c = old column 2m + c + d: lane m + (c + d) / 2,
+            // element (c + d) % 2 (zero past the window)
+            auto slide = [&](double (&acc)[2]) {
+              double nv[2];
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) cf[v][s2] = cn[v][s2];
+              for (int c = 0; c < 2; ++c) {
+                const int ls = (c + d) / 2, el = (c + d) % 2;
+                const double src = el ? acc[1] : acc[0];
+                const double got = __shfl_down_sync(0xffffffffu, src, ls, 4);
+                nv[c] = (m + ls < 4) ? got : 0.0;
+              }
+              acc[0] = nv[0];
+              acc[1] = nv[1];
+            };
+            slide(w00);
+            if (STIFF) {
+              slide(w10);
+              slide(w01);
+            }
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+              for (int s2 = 0; s2 < 2; ++s2) cf[v][s2] = cn[v][s2];
+          }
         }
         widx = widx0 + NBX;
-        // remaining columns [EX, EX + 8): lane m holds EX + 2m + c
+        // remaining columns [c0(last), c0(last) + 8): lane m holds c0 + 2m + c
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int col = EX + 2 * m + c;
+          const int col = C::c0w(NWIN - 1) + 2 * m + c;
           if (col < FX) {
             Crow[col] = w00[c];
             if (STIFF) {
@@ -736,15 +755,15 @@ __global__ void apply_reduce_kernel(const ReduceArgs r) {
 // ---- instantiation table ----------------------------------------------------
 
 struct Launch {
-  int EX, EY, NT, NPL, QE, EPB;
+  int EX, EY, NT, NPL, QE;
   size_t smem;
   void (*kernel)(ApplyArgs, CUtensorMap);
 };
 
-template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2, int EPB = 1>
+template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2>
 Launch make_launch() {
-  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>;
-  return Launch{EX, EY, C::NT, C::NPL, C::QE, EPB, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG, EPB>};
+  using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG>;
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG>};
 }
 
 // Development switch (IGS_APPLY_VARIANT) for comparing tile shapes on the box.
@@ -767,11 +786,9 @@ bool pick(int P, int Q, Launch* L) {
     case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF>(); return true;
     case 4: *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>(); return true;
     case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
-    case 6:
-      // 2-element boxes (96-byte rows: whole sectors, half the TMA issues);
-      // 7 planes do not fit them, single-element boxes in a 3-stage ring
-      if (apply_variant() == 1 || (MASS && STIFF)) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
-      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2, 2>();
+    case 6:  // 7 planes (M+K) fit a 2-stage ring, 6 a 3-stage one
+      if (apply_variant() == 1 || (MASS && STIFF)) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
+      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
       return true;
     case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
     case 8:
@@ -818,13 +835,10 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
   return t;
 }
 
-// L2 promotion of the coefficient boxes: 64-byte box rows (one element of
-// 8 points) gain from 256-byte promotion (the warp's next elements arrive
-// with them: C5 -3 %); wider rows take whole sectors without promotion
-// (C4: DRAM reads = B_alg exactly instead of +3.6 %, same time).
-CUtensorMapL2promotion l2_promotion(const Launch& L) {
-  return L.EPB > 1 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
+// L2 promotion of the coefficient boxes: 64-byte box rows (one 8-point
+// window) gain from 256-byte promotion (the warp's next windows arrive with
+// them: C5 -3 %).
+CUtensorMapL2promotion l2_promotion(const Launch&) { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 
 // The coefficient planes as one 4D tensor (x, y, z points, plane) for TMA.
 // cuTensorMapEncodeTiled comes from the driver through the runtime's entry
