@@ -188,6 +188,42 @@ igs_status igs_write_matrix_market(const char* path /* host */, int64_t nrows, i
                                    const int64_t* indptr /* host */, const int64_t* indices /* host */,
                                    const double* values /* host */);
 
+/* ---- f1: coefficient field from a geometry map ---------- */
+/* Pointwise half of eval_geometry + build_coefficient_field
+ * (geometry.py:158-216 Jacobians, :121-155 cofactor inverse, :315-336
+ * pullback).  The spline fields of the map come from igs_eval_field (Alg. 3)
+ * on the map's own bases tabulated at the quadrature points.  All arrays are
+ * device arrays of npts doubles in the flat point order. */
+typedef struct {
+  int32_t d;                          /* 1..3, physical dimension = d            */
+  int64_t npts;
+  const double* val[IGS_MAX_DIM];     /* G_c (weighted numerator w·G_c if rational) */
+  const double* grad[IGS_MAX_DIM][IGS_MAX_DIM]; /* d/dx_k of val[c]            */
+  const double* wval;                 /* weight spline w (NULL: polynomial map)  */
+  const double* wgrad[IGS_MAX_DIM];   /* d/dx_k of w                             */
+  /* PDE data (geometry.py:219-276): NULL = absent; stride 0 = one constant,
+   * stride 1 = one value per point. */
+  const double* reaction;
+  int64_t reaction_stride;
+  const double* convection[IGS_MAX_DIM];
+  int64_t convection_stride;
+  const double* diffusion[IGS_MAX_DIM][IGS_MAX_DIM];
+  int64_t diffusion_stride;
+  double rtol;                        /* degenerate if |det J| < rtol·max|J|^d (1e-12) */
+} igs_pullback_args;
+
+/* F = |det J|·E·[[c,0],[b,A]]·E^T, E = diag(1, J^{-1}), written as planes:
+ * plane_of (host, [4][4] row-major, eta i x theta j over the first-order
+ * set) maps F[i][j] to a plane (-1: not stored; a plane shared by (i,j) and
+ * (j,i) is written once).  nonzero (device [n_planes]) gets 1 for every plane
+ * holding a non-zero value; phys (device [d][npts] or NULL) the mapped
+ * points.  *bad (host) = first point with a degenerate Jacobian, else -1.
+ * Synchronises the stream (the degeneracy verdict is returned).  ws >= 64 B. */
+igs_status igs_geometry_pullback(const igs_pullback_args* args, const int8_t* plane_of /* host */,
+                                 int32_t n_planes, double* planes, int64_t plane_stride, double* phys,
+                                 uint32_t* nonzero, int64_t* bad /* host */, void* ws, size_t ws_bytes,
+                                 void* stream);
+
 /* ---- K5: halo pack / unpack-add for the slab-partitioned apply ------- */
 /* Copies `nlayers` contiguous DoF layers (layer = N0*N1 doubles) — kept
  * as kernels so they can be captured in CUDA graphs. dst[i] (+)= src[i]. */

@@ -156,6 +156,42 @@ def golden_blocks():
          indptr=prob.pattern().indptr, indices=prob.pattern().indices)
 
 
+AFFINE_M = np.array([[1.0, 0.2, 0.0], [0.0, 1.5, 0.1], [0.3, 0.0, 0.8]])
+AFFINE_B = np.array([0.5, -0.25, 1.0])
+DIFF_M = np.array([[2.0, 0.3, 0.1], [0.3, 1.0, 0.2], [0.1, 0.2, 1.5]])
+
+
+def geometry_cases():
+    """(name, map, elements per direction, points per element, pde) — the
+    tests rebuild the same cases through the repo's API."""
+    return [
+        ("qa", geometry.quarter_annulus(), 3, 3, geometry.pde_convection_diffusion(convection="default")),
+        ("tb", geometry.twisted_box(), 2, 3, geometry.pde_laplace()),
+        ("af", geometry.affine_geometry(AFFINE_M, AFFINE_B), 2, 2,
+         geometry.PDEData(diffusion=DIFF_M, convection=[1.0, -2.0, 0.5], reaction=0.7)),
+        ("qf", geometry.quarter_annulus(0.5, 1.5), 2, 4,
+         geometry.PDEData(diffusion="identity", reaction=lambda x: 1.0 + x[:, 0] ** 2)),
+    ]
+
+
+def golden_geometry():
+    for name, geo, ne, k, pde in geometry_cases():
+        rules = [quadrature.per_element_rule(np.linspace(0.0, 1.0, ne + 1), k) for _ in range(geo.d)]
+        quad = quadrature.TensorQuadrature(rules)
+        ev = geometry.eval_geometry(geo, quad)
+        F = geometry.build_coefficient_field(ev, pde).values
+        save(f"geo_{name}", meta=np.array([geo.d, ne, k]), phys=ev.phys, jac=ev.jac, det=ev.det, inv=ev.inv, F=F)
+    # full pipeline: quarter annulus, p=3 on 4x4 elements, cdr pulled back
+    p, K = 3, 4
+    bases = [bspline.UnivariateBasis(bspline.uniform_open_knots(p, K)) for _ in range(2)]
+    quad = quadrature.TensorQuadrature([quadrature.per_element_rule(b.breakpoints, p) for b in bases])
+    field = geometry.PulledBackCoefficient(geometry.quarter_annulus(), geometry.pde_convection_diffusion(
+        convection="default")).evaluate(quad)
+    A = sumfac.assemble(sumfac.AssemblyProblem(bases, bases, quad, field))
+    save("geo_qa_assembly", meta=np.array([2, p, K]), values=A.values, indptr=A.pattern.indptr,
+         indices=A.pattern.indices)
+
+
 if __name__ == "__main__":
     golden_gauss()
     golden_tabulate()
@@ -163,3 +199,4 @@ if __name__ == "__main__":
     golden_assembly()
     golden_apply()
     golden_blocks()
+    golden_geometry()

@@ -64,6 +64,24 @@ class IgsProblem(ctypes.Structure):
     ]
 
 
+class IgsPullbackArgs(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32),
+        ("npts", ctypes.c_int64),
+        ("val", ctypes.c_void_p * MAX_DIM),
+        ("grad", (ctypes.c_void_p * MAX_DIM) * MAX_DIM),
+        ("wval", ctypes.c_void_p),
+        ("wgrad", ctypes.c_void_p * MAX_DIM),
+        ("reaction", ctypes.c_void_p),
+        ("reaction_stride", ctypes.c_int64),
+        ("convection", ctypes.c_void_p * MAX_DIM),
+        ("convection_stride", ctypes.c_int64),
+        ("diffusion", (ctypes.c_void_p * MAX_DIM) * MAX_DIM),
+        ("diffusion_stride", ctypes.c_int64),
+        ("rtol", ctypes.c_double),
+    ]
+
+
 # (name, restype, argtypes) for every symbol declared in include/igs_capi.h.
 _SIGNATURES = [
     ("igs_last_error", ctypes.c_char_p, []),
@@ -99,6 +117,10 @@ _SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
     ("igs_write_matrix_market", ctypes.c_int,
      [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("igs_geometry_pullback", ctypes.c_int,
+     [ctypes.POINTER(IgsPullbackArgs), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+      ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_size_t,
+      ctypes.c_void_p]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

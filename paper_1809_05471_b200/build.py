@@ -34,6 +34,7 @@ SOURCES = [
     "synth.cu",
     "apply3d.cu",
     "assemble3d.cu",
+    "geometry.cu",
     "mmio.cpp",
 ]
 

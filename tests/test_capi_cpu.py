@@ -86,6 +86,34 @@ int main(void) {
     assert out == want
 
 
+def test_pullback_struct_layout_matches_header():
+    from paper_1809_05471_b200 import _lib
+
+    src = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "igs_capi.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(igs_pullback_args), offsetof(igs_pullback_args, npts),
+         offsetof(igs_pullback_args, grad), offsetof(igs_pullback_args, wval),
+         offsetof(igs_pullback_args, reaction_stride), offsetof(igs_pullback_args, convection),
+         offsetof(igs_pullback_args, diffusion), offsetof(igs_pullback_args, rtol));
+  return 0;
+}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        exe = os.path.join(d, "t")
+        open(c, "w").write(src)
+        r = subprocess.run(["gcc", "-I", os.path.dirname(HEADER), c, "-o", exe], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        out = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
+    A = _lib.IgsPullbackArgs
+    want = [ctypes.sizeof(A), A.npts.offset, A.grad.offset, A.wval.offset, A.reaction_stride.offset,
+            A.convection.offset, A.diffusion.offset, A.rtol.offset]
+    assert out == want
+
+
 def test_package_imports_without_gpu():
     import paper_1809_05471_b200 as pkg
     from paper_1809_05471_b200 import bspline, sharded, tensorspace
