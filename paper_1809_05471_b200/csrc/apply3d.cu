@@ -719,36 +719,35 @@ struct ReduceArgs {
 };
 
 // y[n] = Σ over the work-item boxes covering n, in (tz, ty, tx) order.
-__global__ void apply_reduce_kernel(const ReduceArgs r) {
-  const int64_t total = r.N0 * r.N1 * r.N2;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    int64_t n0 = g % r.N0, n1 = (g / r.N0) % r.N1, n2 = g / (r.N0 * r.N1);
-    int tx_hi = (int)min64(r.ntx - 1, n0 / r.EX);
-    int ty_hi = (int)min64(r.nty - 1, n1 / r.EY);
-    int tz_hi = (int)min64(r.nch - 1, n2 / r.ez);
-    // first tiles whose boxes can still reach n (box extent FX / FY / ez+P-1)
-    int tx_lo = n0 >= r.FX ? (int)((n0 - r.FX) / r.EX + 1) : 0;
-    int ty_lo = n1 >= r.FY ? (int)((n1 - r.FY) / r.EY + 1) : 0;
-    int64_t zspan = (int64_t)r.ez + r.P - 1;
-    int tz_lo = n2 >= zspan ? (int)((n2 - zspan) / r.ez + 1) : 0;
+// Grid (x: n0 blocks, y: n1, z: n2 stride) — 32-bit coordinates, no 64-bit
+// divisions on the per-DoF path.
+__global__ void __launch_bounds__(128) apply_reduce_kernel(const ReduceArgs r) {
+  const int n0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n0 >= r.N0) return;
+  const int EX = r.EX, EY = r.EY, FX = r.FX, FY = r.FY, ez = r.ez;
+  const int tx_hi = min(r.ntx - 1, n0 / EX), tx_lo = n0 >= FX ? (n0 - FX) / EX + 1 : 0;
+  const int zspan = ez + r.P - 1;
+  for (int n1 = blockIdx.y; n1 < r.N1; n1 += gridDim.y)
+  for (int n2 = blockIdx.z; n2 < r.N2; n2 += gridDim.z) {
+    const int ty_hi = min(r.nty - 1, n1 / EY), ty_lo = n1 >= FY ? (n1 - FY) / EY + 1 : 0;
+    const int tz_hi = min(r.nch - 1, n2 / ez), tz_lo = n2 >= zspan ? (n2 - zspan) / ez + 1 : 0;
     double s = 0.0;
     for (int tz = tz_lo; tz <= tz_hi; ++tz) {
-      int64_t z0 = (int64_t)tz * r.ez;
-      int64_t z1 = min64(r.K2, z0 + r.ez);
+      const int z0 = tz * ez, z1 = min(r.K2, z0 + ez);
       if (n2 >= z1 + r.P - 1 || n2 < z0) continue;
       for (int ty = ty_lo; ty <= ty_hi; ++ty) {
-        int64_t l1 = n1 - (int64_t)ty * r.EY;
-        if (l1 >= r.FY) continue;
+        const int l1 = n1 - ty * EY;
+        if (l1 >= FY) continue;
         for (int tx = tx_lo; tx <= tx_hi; ++tx) {
-          int64_t l0 = n0 - (int64_t)tx * r.EX;
-          if (l0 >= r.FX) continue;
-          int64_t item = ((int64_t)tz * r.nty + ty) * r.ntx + tx;
-          s += r.scratch[item * r.box + ((n2 - z0) * r.FY + l1) * r.FX + l0];
+          const int l0 = n0 - tx * EX;
+          if (l0 >= FX) continue;
+          const int64_t item = ((int64_t)tz * r.nty + ty) * r.ntx + tx;
+          s += r.scratch[item * r.box + ((n2 - z0) * FY + l1) * FX + l0];
         }
       }
     }
-    r.y[g] = r.accumulate ? r.y[g] + s : s;
+    const int64_t gi = ((int64_t)n2 * r.N1 + n1) * r.N0 + n0;
+    r.y[gi] = r.accumulate ? r.y[gi] + s : s;
   }
 }
 
@@ -939,10 +938,8 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
   r.ntx = t.ntx; r.nty = t.nty; r.nch = t.nch; r.ez = t.ez; r.K2 = (int)s.nel[2];
   r.box = t.box;
   r.accumulate = (flags & IGS_FLAG_ACCUMULATE) ? 1 : 0;
-  int64_t total = r.N0 * r.N1 * r.N2;
-  int64_t g = ceil_div(total, 256);
-  if (g > 148 * 16) g = 148 * 16;
-  apply_reduce_kernel<<<(unsigned)g, 256, 0, st>>>(r);
+  const dim3 rgrid((unsigned)ceil_div(r.N0, 128), (unsigned)min64(r.N1, 65535), (unsigned)min64(r.N2, 64));
+  apply_reduce_kernel<<<rgrid, 128, 0, st>>>(r);
   IGS_LAUNCH_CHECK("apply_reduce_kernel");
   return IGS_OK;
 }
