@@ -162,6 +162,7 @@ struct Asm3Args {
   int lz;             // z point layers per CTA
   int nplanes;        // planes in the TMA box (all planes of the field)
   int64_t z0, z1;     // global z points to contract: elements [e_lo, e_hi) of the row range
+  int64_t NE;         // elements in H (e_hi - e_lo)
   int64_t zpl;        // global z point of the coefficient planes' first layer (slab origin)
 };
 
@@ -169,6 +170,16 @@ __device__ __forceinline__ void dmma_a(double& d0, double& d1, double a, double 
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// Sweep-blocked layout of the last-direction intermediate (H in 3D, G in
+// 2D): [block of 128 slot pairs][element - e_lo][q][group][128], so one
+// element of one sweep block is a contiguous Q·ngrp·128-double tile (one
+// bulk copy).
+constexpr int kSweepBlock = 128;
+__host__ __device__ __forceinline__ int64_t sweep_offset(int64_t sp, int64_t e_loc, int q, int h, int64_t NE,
+                                                         int Q, int ngrp) {
+  return ((((sp / kSweepBlock) * NE + e_loc) * Q + q) * ngrp + h) * kSweepBlock + sp % kSweepBlock;
 }
 
 // Stage-1/2 tile plan: T x T rows in (x, y), their (T+P-1)-element support
@@ -358,7 +369,8 @@ __global__ void __launch_bounds__(512, 1)
       const int64_t gs0b = (int64_t)(a0 + (s0 + 1) / SR) * W + (s0 + 1) % SR;
       const bool ok0 = row_ok && s0 < PT && s0 % SR < W && gs0 < a.NS0;
       const bool ok1 = row_ok && s0 + 1 < PT && (s0 + 1) % SR < W && gs0b < a.NS0;
-      double* hrow = a.H + ((x2 - a.z0) * nh * a.NS1 + gs1) * a.NS0;
+      const int64_t e_loc = (x2 - a.z0) / Q;
+      const int qz = (int)((x2 - a.z0) % Q);
       const double* Wk = W1 + s1 * YP + m4 + k_lo * 4;
       const double* Gk = Gs + (m4 + k_lo * 4) * SP + st * 8 + g8;
       double d0 = 0.0, d1 = 0.0;
@@ -371,9 +383,9 @@ __global__ void __launch_bounds__(512, 1)
         for (int kk = 0; kk < KL2; ++kk)
           if (k_lo + kk < k_hi) dmma_a(d0, d1, Wg[kk * 4], Gg[kk * 4 * SP]);
         if (g + 1 == pl.ng || pl.g_h[g + 1] != pl.g_h[g]) {
-          double* dst = hrow + (int64_t)pl.g_h[g] * a.NS1 * a.NS0;
-          if (ok0) dst[gs0] = d0;
-          if (ok1) dst[gs0b] = d1;
+          const int h = pl.g_h[g];
+          if (ok0) a.H[sweep_offset(gs1 * a.NS0 + gs0, e_loc, qz, h, a.NE, Q, nh)] = d0;
+          if (ok1) a.H[sweep_offset(gs1 * a.NS0 + gs0b, e_loc, qz, h, a.NE, Q, nh)] = d1;
           d0 = d1 = 0.0;
         }
       }
@@ -393,6 +405,7 @@ struct Asm3bArgs {
   double* values;
   const double* w2g;              // [K][Q][P][P][4] weights of the swept direction
   int e_lo, e_hi;                 // elements swept (H holds their points from e_lo·Q)
+  int64_t NE;                     // elements held by H (sweep-blocked layout)
   int chunk;                      // elements per thread chunk (rows written per chunk)
   int ngrp;                       // groups summed per point (3D: nh, 2D: ng)
   int grp_v[4];                   // their variant codes in the swept direction
@@ -420,49 +433,48 @@ __global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
   w2g[i] = val;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dev::smem_u32(dst)), "l"(src) : "memory");
-}
 
-// Stage-3 pipeline: shared-memory ring of NS3 element stages, prefetched
-// D3 = NS3 - 2 elements ahead with cp.async (no registers held by loads).
-constexpr int NS3 = 4, D3 = NS3 - 2, NT3 = 128;
+// Last-direction pipeline: shared-memory ring of NS3 element stages, each
+// filled by two bulk copies (the block's H tile and the element weights)
+// D3 = NS3 - 2 elements ahead.
+constexpr int NS3 = 4, D3 = NS3 - 2, NT3 = kSweepBlock;
 template <int P, int Q>
 struct S3Cfg {
   static constexpr int NWT = Q * P * P * 4;   // weights per element
-  static constexpr int HST = Q * 4 * NT3;     // H values per stage [q][h][thread]
-  static constexpr size_t SMEM = (size_t)NS3 * (HST + NWT) * sizeof(double);
+  static constexpr int HST = Q * 4 * NT3;     // H values per stage [q][group <= 4][thread]
+  static constexpr size_t SMEM = (size_t)NS3 * (HST + NWT) * sizeof(double) + NS3 * sizeof(uint64_t);
 };
 
-// Last-direction sweep (3D stage 3, 2D stage 2).  One thread per (slot0[,
-// slot1], chunk of elements) sweeps the last direction with a ring of P rows
-// x (2P-1) cols in registers.  Each thread streams its own H values (Q
-// points x 4 groups per element) into a private column of the shared stage
-// ring; the element weights stream into the same ring slot, published by one
-// barrier per element, so HBM reads stay D3 elements ahead of the
-// contraction.  A chunk starts P-1 elements early (its first rows are then
-// complete) and writes the rows of its own elements (the last chunk also the
-// trailing P-1 rows).  2D is 3D with a trivial middle direction.
+// Last-direction sweep (3D stage 3, 2D stage 2).  Block = (chunk of
+// elements, 128 consecutive slot pairs (slot0[, slot1])); each thread sweeps
+// the last direction for its pair with a ring of P rows x (2P-1) cols in
+// registers.  An element's H values for the whole block are one contiguous
+// tile of the sweep-blocked layout, fetched with the element's weights by
+// one thread (cp.async.bulk + mbarrier) D3 elements ahead.  A chunk starts
+// P-1 elements early (its first rows are then complete) and writes the rows
+// of its own elements (the last chunk also the trailing P-1 rows).  2D is
+// 3D with a trivial middle direction.
 template <int P, int Q, int D>
 __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs a) {
   using C = S3Cfg<P, Q>;
   constexpr int W = 2 * P - 1, NWT = C::NWT, L = D - 1;
   static_assert(NWT % 2 == 0, "16-byte table chunks");
   extern __shared__ __align__(16) double s3[];
-  double* hst = s3;                    // [NS3][Q][4][NT3]
+  double* hst = s3;                    // [NS3][Q][ngrp][NT3]
   double* w2s = s3 + NS3 * C::HST;     // [NS3][Q][P][P][4]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWT);
   const int nh = a.ngrp;
   const int tid = threadIdx.x;
-  const int64_t gid = blockIdx.x * (int64_t)NT3 + tid;
   const int64_t npairs = a.NS0 * a.NS1;
-  const int64_t sp = gid % npairs, chunk_id = gid / npairs;
+  const int64_t nbsp = (npairs + NT3 - 1) / NT3;
+  const int chunk_id = (int)(blockIdx.x / nbsp);
+  const int64_t sb = blockIdx.x % nbsp;
+  const int64_t sp = sb * NT3 + tid;
   const int64_t s0 = sp % a.NS0, s1 = sp / a.NS0;
-  const int nchunk = (a.e_hi - a.e_lo + a.chunk - 1) / a.chunk;
-  const bool live = chunk_id < nchunk;
   const int64_t N0 = a.tab.N[0], N1 = D == 3 ? a.tab.N[1] : 1, N2 = a.tab.N[L];
   const int64_t m0 = s0 / W, n0 = m0 + (s0 % W) - (P - 1);
   const int64_t m1 = D == 3 ? s1 / W : 0, n1 = D == 3 ? m1 + (s1 % W) - (P - 1) : 0;
-  const bool valid = live && n0 >= 0 && n0 < N0 && n1 >= 0 && n1 < N1 && m0 < N0 && m1 < N1;
+  const bool valid = sp < npairs && n0 >= 0 && n0 < N0 && n1 >= 0 && n1 < N1 && m0 < N0 && m1 < N1;
   // CSR geometry of this thread's (row, column) pairs in the first directions
   int64_t w0 = 1, w1 = 1, rp0 = 0, rp1 = 0, r0 = 0, r1 = 0, P0 = 1, P1 = 1;
   if (valid) {
@@ -483,8 +495,8 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
 #pragma unroll
     for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
   const int K2 = a.tab.K[L];
-  // this chunk's elements [c_lo, c_hi) and rows [c_lo, c_hi) (+ trailing rows)
-  const int c_lo = a.e_lo + (live ? (int)chunk_id : 0) * a.chunk;
+  // this block's chunk: rows [c_lo, c_hi) (+ trailing rows), elements from c_lo - P + 1
+  const int c_lo = a.e_lo + chunk_id * a.chunk;
   const int c_hi = min(a.e_hi, c_lo + a.chunk);
   const int e_lo = max(a.e_lo, c_lo - (P - 1)), e_hi = c_hi;
   auto flush = [&](int64_t m2, const double* row) {
@@ -501,89 +513,69 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       if (n2 >= 0 && n2 < N2) a.values[start + (n2 - lo2) * w0 * w1 + r1 * w0 + r0] = row[k];
     }
   };
-  const int64_t hs = npairs;  // stride between (point, group) planes
-  const double* hbase = a.H + (valid ? sp : 0);
-  // The block's threads share one chunk range except at chunk boundaries
-  // inside the block: the stage ring, the weights and the barriers follow
-  // the block-wide range [blk_lo, blk_hi); a thread copies and contracts H
-  // only for the elements of its own range [e_lo, e_hi).
-  const int64_t gid0 = blockIdx.x * (int64_t)NT3, gid1 = gid0 + NT3 - 1;
-  const int cb0 = (int)min64(gid0 / npairs, nchunk - 1), cb1 = (int)min64(gid1 / npairs, nchunk - 1);
-  const int blk_lo = max(a.e_lo, a.e_lo + cb0 * a.chunk - (P - 1));
-  const int blk_hi = min(a.e_hi, a.e_lo + (cb1 + 1) * a.chunk);
-  // element e2 -> stage (e2 - blk_lo) % NS3: this thread's H column + its share of the weights
-  auto issue = [&](int e2) {
-    if (e2 < blk_hi) {
-      const int stg = (e2 - blk_lo) % NS3;
-      if (e2 >= e_lo && e2 < e_hi) {
-        const double* hp = hbase + (int64_t)(e2 - a.e_lo) * Q * nh * hs;
-        double* hd = hst + stg * C::HST + tid;
-#pragma unroll
-        for (int q = 0; q < Q; ++q)
-#pragma unroll
-          for (int hh = 0; hh < 4; ++hh) {
-            const bool ok = valid && hh < nh;
-            const unsigned d = dev::smem_u32(hd + (q * 4 + hh) * NT3);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
-                         "l"(ok ? hp + (q * nh + hh) * hs : a.H), "r"(ok ? 8 : 0)
-                         : "memory");
-          }
-      }
-      const double* src = a.w2g + (int64_t)e2 * NWT;
-      double* dst = w2s + stg * NWT;
-      for (int i = tid; i < NWT / 2; i += NT3) cp_async16(dst + 2 * i, src + 2 * i);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group per element
+  const unsigned htile = (unsigned)(Q * nh * NT3 * sizeof(double));
+  const unsigned wbytes = (unsigned)(NWT * sizeof(double));
+  const double* hblock = a.H + sb * a.NE * Q * nh * NT3;
+  auto issue = [&](int e2) {  // one thread
+    if (e2 >= e_hi) return;
+    const int stg = (e2 - e_lo) % NS3;
+    dev::mbar_expect_tx(bars + stg, htile + wbytes);
+    dev::bulk_load(hst + stg * C::HST, hblock + (int64_t)(e2 - a.e_lo) * Q * nh * NT3, htile, bars + stg);
+    dev::bulk_load(w2s + stg * NWT, a.w2g + (int64_t)e2 * NWT, wbytes, bars + stg);
   };
-  // rebase the ring so slot (m2 - blk_lo) % P is static per unrolled step
-#pragma unroll
-  for (int e = 0; e < D3; ++e) issue(blk_lo + e);
-  for (int eb = blk_lo; eb < blk_hi; eb += P) {
+  if (tid < NS3) dev::mbar_init(bars + tid, 1);
+  dev::fence_mbar_init();
+  __syncthreads();
+  if (tid == 0)
+    for (int e = 0; e < D3; ++e) issue(e_lo + e);
+  for (int eb = e_lo; eb < e_hi; eb += P) {
 #pragma unroll
     for (int r = 0; r < P; ++r) {  // ring row of element e2 is static: r
       const int e2 = eb + r;
-      if (e2 >= blk_hi) break;
-      // stage (e2 + D3 - blk_lo) % NS3 was last read for element e2 - 2,
-      // finished by every thread before the barrier of element e2 - 1
-      issue(e2 + D3);
-      asm volatile("cp.async.wait_group %0;" ::"n"(D3) : "memory");
-      __syncthreads();  // element e2's weights (copied by the threads that own it) visible
-      if (e2 >= e_lo && e2 < e_hi) {
-        const int stg = (e2 - blk_lo) % NS3;
-        const double* hcol = hst + stg * C::HST + tid;
-        const double* wst = w2s + stg * NWT;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const double h0 = hcol[(q * 4 + 0) * NT3], h1 = hcol[(q * 4 + 1) * NT3];
-          const double h2 = hcol[(q * 4 + 2) * NT3], h3 = hcol[(q * 4 + 3) * NT3];
-#pragma unroll
-          for (int jm = 0; jm < P; ++jm)
-#pragma unroll
-            for (int jn = 0; jn < P; ++jn) {
-              const double2 wa = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4);
-              const double2 wb = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4 + 2);
-              double sacc = ring[(r + jm) % P][jn - jm + P - 1];
-              sacc = fma(wa.x, h0, sacc);
-              sacc = fma(wa.y, h1, sacc);
-              sacc = fma(wb.x, h2, sacc);
-              sacc = fma(wb.y, h3, sacc);
-              ring[(r + jm) % P][jn - jm + P - 1] = sacc;
-            }
-        }
-        // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
-        if (valid) flush(e2, ring[r]);
+      if (e2 >= e_hi) break;
+      // stage (e2 + D3 - e_lo) % NS3 was last read for element e2 - 2,
+      // finished by every thread before this barrier
+      __syncthreads();
+      if (tid == 0) {
+        dev::fence_proxy_async();
+        issue(e2 + D3);
       }
+      const int stg = (e2 - e_lo) % NS3;
+      dev::mbar_wait(bars + stg, (unsigned)(((e2 - e_lo) / NS3) & 1));
+      const double* hcol = hst + stg * C::HST + tid;
+      const double* wst = w2s + stg * NWT;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const double h0 = hcol[(q * nh + 0) * NT3];
+        const double h1 = nh > 1 ? hcol[(q * nh + 1) * NT3] : 0.0;
+        const double h2 = nh > 2 ? hcol[(q * nh + 2) * NT3] : 0.0;
+        const double h3 = nh > 3 ? hcol[(q * nh + 3) * NT3] : 0.0;
+#pragma unroll
+        for (int jm = 0; jm < P; ++jm)
+#pragma unroll
+          for (int jn = 0; jn < P; ++jn) {
+            const double2 wa = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4);
+            const double2 wb = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4 + 2);
+            double sacc = ring[(r + jm) % P][jn - jm + P - 1];
+            sacc = fma(wa.x, h0, sacc);
+            sacc = fma(wa.y, h1, sacc);
+            sacc = fma(wb.x, h2, sacc);
+            sacc = fma(wb.y, h3, sacc);
+            ring[(r + jm) % P][jn - jm + P - 1] = sacc;
+          }
+      }
+      // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
+      if (valid) flush(e2, ring[r]);
 #pragma unroll
       for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
     }
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
   // trailing rows m2 in [K2, K2 + P - 1) (their last element is K2 - 1)
   if (valid && e_hi == K2) {
 #pragma unroll
     for (int t = 1; t < P; ++t) {
       const int64_t m2 = K2 - 1 + t;
-      const int slot = (int)((m2 - blk_lo) % P);
+      const int slot = (int)((m2 - e_lo) % P);
 #pragma unroll
       for (int s = 0; s < P; ++s)
         if (s == slot) flush(m2, ring[s]);
@@ -596,8 +588,9 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
 struct Asm2Args {
   AsmPlan plan;
   TabArgs tab;
-  double* G;       // [X1][ng][NS0]
+  double* G;       // sweep-blocked [NS0 blocks][K1][Q][ng][128]
   int64_t NS0;
+  int64_t NE;      // elements of the last direction (K1)
   int nt0;         // row tiles in x
   int yc;          // y points per CTA (multiple of A2_YS)
 };
@@ -678,9 +671,9 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
         for (int kk = 0; kk < KL; ++kk)
           if (k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
         if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
-          double* dst = a.G + (y * pl.ng + pl.b_g[b]) * a.NS0;
-          if (ok0) dst[gs0] = d0;
-          if (ok1) dst[gs0b] = d1;
+          const int gq = (int)(y % Q), h = pl.b_g[b];
+          if (ok0) a.G[sweep_offset(gs0, y / Q, gq, h, a.NE, Q, pl.ng)] = d0;
+          if (ok1) a.G[sweep_offset(gs0b, y / Q, gq, h, a.NE, Q, pl.ng)] = d1;
           d0 = d1 = 0.0;
         }
       }
@@ -798,11 +791,12 @@ TabArgs tab_args(const igs_problem* p) {
 
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
+  auto padded = [](int64_t n) { return (size_t)ceil_div(n, (int64_t)kSweepBlock) * kSweepBlock; };
   if (s.fs.d == 3) {
-    return (size_t)s.zpts * s.plan.nh * (s.fs.nfn[1] * W) * (s.fs.nfn[0] * W) * sizeof(double) +
+    return padded((s.fs.nfn[1] * W) * (s.fs.nfn[0] * W)) * s.zpts * s.plan.nh * sizeof(double) +
            (size_t)s.fs.nel[2] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
   }
-  return (size_t)s.fs.npt[1] * s.plan.ng * (s.fs.nfn[0] * W) * sizeof(double) +
+  return padded(s.fs.nfn[0] * W) * s.fs.npt[1] * s.plan.ng * sizeof(double) +
          (size_t)s.fs.nel[1] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
 }
 
@@ -854,6 +848,7 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const ZRange
   }
   a.z0 = (int64_t)z.e_lo * Q;
   a.z1 = (int64_t)z.e_hi * Q;
+  a.NE = z.e_hi - z.e_lo;
   a.zpl = (int64_t)z.sl * Q;
   // z chunks: enough CTAs for ~4 waves at one CTA per SM
   const int64_t tiles = (int64_t)a.nt0 * a.nt1;
@@ -899,7 +894,8 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.values = values;
   b.base = base;
   // stage-3 weights after H in the workspace (H sized for the slab / grid)
-  double* w2g = H + (size_t)(z.sh - z.sl) * Q * s.plan.nh * a.NS1 * a.NS0;
+  const int64_t nbsp = ceil_div(a.NS0 * a.NS1, (int64_t)kSweepBlock);
+  double* w2g = H + (size_t)nbsp * kSweepBlock * (z.sh - z.sl) * Q * s.plan.nh;
   b.w2g = w2g;
   b.e_lo = z.e_lo;
   b.e_hi = z.e_hi;
@@ -911,12 +907,12 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
     asm_wlast_kernel<P, Q, 3><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);
     IGS_LAUNCH_CHECK("asm_wlast_kernel");
   }
-  int64_t threads = a.NS0 * a.NS1;
+  b.NE = z.e_hi - z.e_lo;
   constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem3),
                      "smem attribute"));
-  asm_sweep<P, Q, 3><<<(unsigned)ceil_div(threads, NT3), NT3, smem3, st>>>(b);
+  asm_sweep<P, Q, 3><<<(unsigned)nbsp, NT3, smem3, st>>>(b);
   IGS_LAUNCH_CHECK("asm_sweep<3>");
   return IGS_OK;
 }
@@ -930,6 +926,7 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
   a.tab = tab_args(p);
   a.G = G;
   a.NS0 = s.fs.nfn[0] * C::W;
+  a.NE = s.fs.nel[1];
   a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
   const size_t smem = A2Cfg<P, Q, T>::smem(p->n_planes);
   if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
@@ -980,7 +977,9 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.base = base;
   b.values = values;
   const int K1 = (int)s.fs.nel[1];
-  double* wlg = G + (size_t)s.fs.npt[1] * s.plan.ng * a.NS0;
+  const int64_t nbsp = ceil_div(a.NS0, (int64_t)kSweepBlock);
+  double* wlg = G + (size_t)nbsp * kSweepBlock * s.fs.npt[1] * s.plan.ng;
+  b.NE = K1;
   b.w2g = wlg;
   b.e_lo = 0;
   b.e_hi = K1;
@@ -998,12 +997,11 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
     asm_wlast_kernel<P, Q, 2><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, wlg);
     IGS_LAUNCH_CHECK("asm_wlast_kernel");
   }
-  const int64_t threads = a.NS0 * ceil_div(K1, chunk);
   constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem3),
                      "smem attribute"));
-  asm_sweep<P, Q, 2><<<(unsigned)ceil_div(threads, NT3), NT3, smem3, st>>>(b);
+  asm_sweep<P, Q, 2><<<(unsigned)(nbsp * ceil_div(K1, chunk)), NT3, smem3, st>>>(b);
   IGS_LAUNCH_CHECK("asm_sweep<2>");
   return IGS_OK;
 }
