@@ -371,6 +371,8 @@ __global__ void __launch_bounds__(512, 1)
       const bool ok1 = row_ok && s0 + 1 < PT && (s0 + 1) % SR < W && gs0b < a.NS0;
       const int64_t e_loc = (x2 - a.z0) / Q;
       const int qz = (int)((x2 - a.z0) % Q);
+      const int64_t off0 = sweep_offset(gs1 * a.NS0 + gs0, e_loc, qz, 0, a.NE, Q, nh);
+      const int64_t off1 = sweep_offset(gs1 * a.NS0 + gs0b, e_loc, qz, 0, a.NE, Q, nh);
       const double* Wk = W1 + s1 * YP + m4 + k_lo * 4;
       const double* Gk = Gs + (m4 + k_lo * 4) * SP + st * 8 + g8;
       double d0 = 0.0, d1 = 0.0;
@@ -383,9 +385,9 @@ __global__ void __launch_bounds__(512, 1)
         for (int kk = 0; kk < KL2; ++kk)
           if (k_lo + kk < k_hi) dmma_a(d0, d1, Wg[kk * 4], Gg[kk * 4 * SP]);
         if (g + 1 == pl.ng || pl.g_h[g + 1] != pl.g_h[g]) {
-          const int h = pl.g_h[g];
-          if (ok0) a.H[sweep_offset(gs1 * a.NS0 + gs0, e_loc, qz, h, a.NE, Q, nh)] = d0;
-          if (ok1) a.H[sweep_offset(gs1 * a.NS0 + gs0b, e_loc, qz, h, a.NE, Q, nh)] = d1;
+          const int hoff = pl.g_h[g] * kSweepBlock;
+          if (ok0) a.H[off0 + hoff] = d0;
+          if (ok1) a.H[off1 + hoff] = d1;
           d0 = d1 = 0.0;
         }
       }
