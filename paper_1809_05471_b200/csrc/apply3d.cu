@@ -260,15 +260,17 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   const int ntask = (z1 - z0) * NB * NBX;
   uint64_t* mybar = bars + warp * STG;
   double* mystage = Fs + warp * STG * FST;
-  auto issue = [&](int idx) {  // one lane: box idx = (batch, window)
-    const int batch = idx / NBX, bx = idx % NBX;
-    const int zq = (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq;
-    uint64_t* bar = mybar + idx % STG;
+  // one lane: box of window bx of point layer zq into ring stage stg
+  const bool co = a.l2pf < 0;  // compute-only measurement mode
+  const int tma_x = ex0 * Q, tma_y = ey0 * Q + wlg * 8;
+  auto issue_box = [&](int stg, int bx, int zq) {
+    uint64_t* bar = mybar + stg;
     mbar_expect_tx(bar, (unsigned)(FST * sizeof(double)));
-    if (a.l2pf < 0)
-      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, ex0 * Q, ey0 * Q + wlg * 8, 0, 0);
-    else
-      tma_load_4d(mystage + (idx % STG) * FST, &fmap, bar, ex0 * Q + bx * 8, ey0 * Q + wlg * 8, zq, 0);
+    tma_load_4d(mystage + stg * FST, &fmap, bar, co ? tma_x : tma_x + bx * 8, tma_y, co ? 0 : zq, 0);
+  };
+  auto issue = [&](int idx) {  // box idx = (batch, window)
+    const int batch = idx / NBX, bx = idx % NBX;
+    issue_box(idx % STG, bx, (z0 + batch / NB) * Q + (batch % NB) * Q2B + wq);
   };
   // lanes past the box width of odd Q read neighbouring stage memory (masked
   // by zero weights): keep it finite
@@ -476,6 +478,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         const bool line_ok = (ey0 + line / Q) < a.K1;
         const double wyz = Wz[q2] * Wy[line];
         const int widx0 = widx;         // = batch·NBX
+        // point layers (slab-local) of this batch's and the next batch's boxes
+        const int zq_cur = e2 * Q + b * Q2B + wq;
+        const int zq_next = b + 1 < NB ? zq_cur + Q2B : (e2 + 1) * Q + wq;
         int stage = 0;                  // ring stage of the current box
         // running X^T window over DoF columns [c0(w), c0(w) + 8): lane m holds
         // c0 + 2m, c0 + 2m + 1
@@ -591,7 +596,12 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           // every lane's reads of this stage have been consumed (the MMAs above
           // depend on them): hand the stage to the next box of this warp
           __syncwarp();
-          if (lane == 0 && widx0 + w + STG < ntask) issue(widx0 + w + STG);
+          if (lane == 0 && widx0 + w + STG < ntask) {
+            // box w + STG of this row: window (w + STG) % NBX of this or the next batch
+            const int nxt = w + STG;
+            const int stg = kStaticRing ? nxt % STG : (widx0 + nxt) % STG;
+            issue_box(stg, nxt % NBX, nxt < NBX ? zq_cur : zq_next);
+          }
           // columns [c0, c0 + d) are complete (no later window touches them):
           // store them over C's columns, which no later window reads, then
           // slide the accumulator window by d columns.
