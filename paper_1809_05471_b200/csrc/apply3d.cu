@@ -201,7 +201,7 @@ struct Cfg {
   static constexpr int CQL = TY * RP;          // one C/R variant plane
   static constexpr int CQ = Q2B * NV * CQL;    // C, overwritten in place by R
   static constexpr int YR = P * LXR;           // y ring
-  static constexpr int TBX = NWIN * 128, TBY = EY * 128, TBZ = 256;  // Tw [w][v][c8][pt8]; Ty/Tz [e][v][q8][j8]
+  static constexpr int TBX = NWIN * 256, TBY = EY * 128, TBZ = 256;  // Tw [w][4][lane][2]; Ty/Tz [e][v][q8][j8]
   static constexpr int WW = TX + TY + 16;
   static constexpr int FS = NW * STG * FST;    // coefficient staging
   static constexpr int TOTAL = FS + XR + AQ + CQ + YR + TBX + TBY + TBZ + WW;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // C, then R in place, then the warp's Y^T partials S_v over its own rows
   double* Cq = Aq + C::AQ;      // [Q2B][NV][TY][RP]
   double* Yr = Cq + C::CQ;      // [P][FYP][RP]
-  double* Tw = Yr + C::YR;      // [NWIN][2][8 c][8 pt]  window tables
+  double* Tw = Yr + C::YR;      // [NWIN][4][32 lanes][2]  window table fragments
   double* Ty = Tw + C::TBX;     // [EY][2][8][8]
   double* Tzb = Ty + C::TBY;    // [2 buffers][2][8][8]
   double* Wx = Tzb + C::TBZ;    // [TX]
@@ -285,13 +285,19 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // ---- prologue ---------------------------------------------------------------
   for (int i = tid; i < C::TOTAL - C::FS; i += NT) Xr[i] = 0.0;  // all MMA padding is zero
   __syncthreads();
-  // Tw[w][v][c][pt] = B^v of DoF column c0(w) + c at window point pt (zero
-  // outside the support or past the mesh)
-  for (int i = tid; i < NWIN * 128; i += NT) {
-    const int pt = i % 8, c = (i / 8) % 8, v = (i / 64) % 2, w = i / 128;
+  // Window table fragments in lane order (one 16-byte load per pair):
+  // B^v(c, pt) = B^v of DoF column c0(w) + c at window point pt (zero outside
+  // the support or past the mesh); pair kp = 0, 1: forward B^v[c = m + 4s][pt
+  // = g] (v = kp), kp = 2, 3: transpose B^v[pt = 2m + s][c = g] (v = kp - 2).
+  for (int i = tid; i < NWIN * 256; i += NT) {
+    const int s = i % 2, ln = (i / 2) % 32, kp = (i / 64) % 4, w = i / 256;
+    const int lg = ln >> 2, lm = ln & 3, v = kp & 1;
+    const int c = kp < 2 ? lm + 4 * s : lg, pt = kp < 2 ? lg : 2 * lm + s;
     const int el = (8 * w + pt) / Q, j = (8 * w) / Q + c - el, ge = ex0 + el;
-    if (ge < a.K0 && j >= 0 && j < P)
-      Tw[i] = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ex0 * Q + 8 * w + pt];
+    double val = 0.0;
+    if (ge < a.K0 && j >= 0 && j < P && (v == 0 || STIFF))
+      val = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ex0 * Q + 8 * w + pt];
+    Tw[i] = val;
   }
   for (int i = tid; i < EY * 2 * Q * P; i += NT) {
     int j = i % P, q = (i / P) % Q, v = (i / (P * Q)) % 2, e = i / (2 * P * Q);
@@ -491,14 +497,20 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         // hoisted when the tile is interior and every window has one pattern
         double fb0[2], fb1[2], tb0[2], tb1[2];
         auto load_tab = [&](int w) {
-          const double* T0 = Tw + (w * 2 + 0) * 64;
-          const double* T1 = Tw + (w * 2 + 1) * 64;
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            fb0[s] = T0[(m + 4 * s) * 8 + g];
-            fb1[s] = STIFF ? T1[(m + 4 * s) * 8 + g] : 0.0;
-            tb0[s] = T0[g * 8 + 2 * m + s];
-            tb1[s] = STIFF ? T1[g * 8 + 2 * m + s] : 0.0;
+          const double2* T = reinterpret_cast<const double2*>(Tw + w * 256) + lane;
+          const double2 f0 = T[0], t0 = T[64];
+          fb0[0] = f0.x;
+          fb0[1] = f0.y;
+          tb0[0] = t0.x;
+          tb0[1] = t0.y;
+          if (STIFF) {
+            const double2 f1 = T[32], t1 = T[96];
+            fb1[0] = f1.x;
+            fb1[1] = f1.y;
+            tb1[0] = t1.x;
+            tb1[1] = t1.y;
+          } else {
+            fb1[0] = fb1[1] = tb1[0] = tb1[1] = 0.0;
           }
         };
         const bool hoist = tile_uniform && C::PER == 1;
@@ -571,9 +583,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           }
           // pointwise (the x weight is zero past the mesh)
           double g0[2], gx[2], gy[2], gz[2];
+          const double2 wx2 = *reinterpret_cast<const double2*>(Wx + 8 * w + 2 * m);
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const double wt = wl * Wx[8 * w + 2 * m + c];
+            const double wt = wl * (c == 0 ? wx2.x : wx2.y);
             if (MASS) g0[c] = wt * (fv[0][c] * u[c]);
             if (STIFF) {
               const double f00 = fv[1][c], f11 = fv[2][c], f22 = fv[3][c];
