@@ -232,3 +232,58 @@ def test_fused_apply_all_orders_vs_oracle(cuda, p, kind):
     # whenever the x point count is even (else the generic kernels run)
     if p != 7 and (p * K[0]) % 2 == 0:
         assert op.fused, f"fused path expected for p={p}"
+
+
+@pytest.mark.parametrize("p,K", [(2, (1, 1, 1)), (4, (1, 2, 3)), (6, (2, 1, 5)), (8, (3, 2, 1)), (7, (2, 4, 2)),
+                                 (6, (24, 17, 2))])
+@pytest.mark.parametrize("kind", [2, 3])
+def test_apply_tiny_and_ragged_meshes_vs_oracle(cuda, p, K, kind):
+    """Meshes smaller than one tile (every element masked but one) and tiles
+    cut by the mesh edge in every direction: fused (when the x rows are
+    16-byte aligned) and generic paths against the oracle."""
+    *_, sumfac, matfree, workloads = _pkg()
+    from paper_1809_05471_b200.bspline import UnivariateBasis, uniform_open_knots
+    from paper_1809_05471_b200.quadrature import TensorQuadrature, per_element_rule
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
+
+    bases = [UnivariateBasis(uniform_open_knots(p, k)) for k in K]
+    quad = TensorQuadrature([per_element_rule(b.breakpoints, p) for b in bases])
+    planes = workloads.synthetic_planes(3, list(quad.shape), kind, seed=31)
+    prob = AssemblyProblem(bases, bases, quad, workloads.field_from_planes(3, kind, planes, quad.shape))
+    x = O.recipe_x(prob.shape[1], seed=8)
+    sp = [O.uniform_space(p, k) for k in K]
+    ths = O.first_order_set(3)
+    y_ref = O.apply(sp, p, ths, ths, O.plane_map(3, kind), planes.cpu().numpy(), x)
+    for generic in (False, True):
+        op = matfree.MatrixFreeOperator(prob, force_generic=generic)
+        assert rel(matfree.apply(op, x), y_ref) <= 1e-12
+        if not generic and (p * K[0]) % 2 == 0:
+            assert op.fused
+
+
+@pytest.mark.parametrize("d,p,K,kind", [(3, 2, (1, 1, 1), 3), (3, 4, (1, 2, 3), 3), (3, 3, (2, 5, 1), 2),
+                                        (3, 5, (2, 1, 2), 3), (3, 6, (1, 1, 2), 2), (2, 5, (1, 3), 3),
+                                        (2, 4, (9, 1), 1)])
+def test_assembly_tiny_and_ragged_meshes_vs_oracle(cuda, d, p, K, kind):
+    """Assembly on meshes smaller than one row tile, fused and generic, against
+    the oracle's independent Kronecker assembly (pattern identical)."""
+    *_, sumfac, matfree, workloads = _pkg()
+    from paper_1809_05471_b200.bspline import UnivariateBasis, uniform_open_knots
+    from paper_1809_05471_b200.quadrature import TensorQuadrature, per_element_rule
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
+
+    bases = [UnivariateBasis(uniform_open_knots(p, k)) for k in K]
+    quad = TensorQuadrature([per_element_rule(b.breakpoints, p) for b in bases])
+    planes = workloads.synthetic_planes(d, list(quad.shape), kind, seed=41)
+    prob = AssemblyProblem(bases, bases, quad, workloads.field_from_planes(d, kind, planes, quad.shape))
+    sp = [O.uniform_space(p, k) for k in K]
+    ths = O.first_order_set(d)
+    F = O.dense_field(planes.cpu().numpy(), O.plane_map(d, kind))
+    Ar = O.assemble_kron(sp, sp, ths, ths, F)
+    pairs = [O.pattern_1d(s.lo, s.hi, s.lo, s.hi, s.points) for s in sp]
+    indptr, indices = O.tensor_csr(pairs, [s.num_basis for s in sp], [s.num_basis for s in sp])
+    ref = O.values_on_pattern(Ar, indptr, indices)
+    for generic in (False, True):
+        A = sumfac._run_assembly(prob, None, None, None, 1 if generic else 0)
+        np.testing.assert_array_equal(prob.pattern().indptr, indptr)
+        assert rel(A.cpu().numpy(), ref) <= 1e-12
