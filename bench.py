@@ -349,21 +349,17 @@ def main():
         except Exception:
             traffic = None
 
-    # --- end to end through the public API: pinned host x -> device -> apply -> host y
+    # --- end to end through the public API: pinned host x -> device -> apply
+    # -> host y every step, transfers overlapped with the neighbouring steps'
+    # applies (matfree.HostPipeline: copy streams + events)
     x_host = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
     x_host.copy_(x_own.cpu())
-    y_host = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
-    x_dev = torch.empty_like(x_own)
-    for _ in range(2):
-        x_dev.copy_(x_host, non_blocking=True)
-        step(x_dev, y_own)
-        y_host.copy_(y_own, non_blocking=True)
+    y_hosts = [torch.empty(n_own, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    pipe = matfree.HostPipeline(step, n_own, n_own)
+    pipe.run([x_host] * 2, y_hosts)
     barrier()
     e0.record()
-    for _ in range(args.steps):
-        x_dev.copy_(x_host, non_blocking=True)
-        step(x_dev, y_own)
-        y_host.copy_(y_own, non_blocking=True)
+    pipe.run([x_host] * args.steps, [y_hosts[i & 1] for i in range(args.steps)])
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)

@@ -17,7 +17,7 @@ from . import _lib
 from .sumfac import FlopCounter
 from .tensorspace import field_eval_count
 
-__all__ = ("MatrixFreeOperator", "apply", "eval_field")
+__all__ = ("MatrixFreeOperator", "apply", "eval_field", "HostPipeline")
 
 
 class MatrixFreeOperator:
@@ -141,6 +141,57 @@ def eval_field(op, u, theta, counter=None):
 
     p = op.problem if isinstance(op, MatrixFreeOperator) else op
     return contract_to_points(p.trial_tables(), theta, u, counter)
+
+
+
+class HostPipeline:
+    """Applies to a sequence of pinned host vectors with the transfers
+    overlapped (CUDA streams): the upload of vector i+1 and the download of
+    result i-1 run on two copy streams while apply i runs on the compute
+    stream; device buffers are double-buffered and ordered by events.
+
+    `step(x_dev, y_dev)` enqueues one apply on the current stream (e.g.
+    ``op.apply_device`` or a sharded step).  Every vector still crosses the
+    bus each step; only the latency of the copies is hidden.
+    """
+
+    def __init__(self, step, n_in, n_out, device="cuda"):
+        torch = _lib.require_cuda()
+        self.step = step
+        self.x = [torch.empty(n_in, dtype=torch.float64, device=device) for _ in range(2)]
+        self.y = [torch.empty(n_out, dtype=torch.float64, device=device) for _ in range(2)]
+        self.up = torch.cuda.Stream(device=device)
+        self.down = torch.cuda.Stream(device=device)
+        self.ev_up = [torch.cuda.Event() for _ in range(2)]
+        self.ev_done = [torch.cuda.Event() for _ in range(2)]
+        self.ev_down = [torch.cuda.Event() for _ in range(2)]
+        self.ev_free = [torch.cuda.Event() for _ in range(2)]
+        for e in self.ev_down + self.ev_free:
+            e.record()
+
+    def run(self, xs_host, ys_host):
+        """ys_host[i] = A xs_host[i] for every i (pinned CPU tensors); returns
+        when every download is enqueued (synchronise before reading)."""
+        torch = _lib.require_cuda()
+        comp = torch.cuda.current_stream()
+        self.up.wait_stream(comp)  # nothing is uploaded before the call
+        for i, (xh, yh) in enumerate(zip(xs_host, ys_host)):
+            k = i & 1
+            with torch.cuda.stream(self.up):
+                self.up.wait_event(self.ev_free[k])   # apply i-2 done with x[k]
+                self.x[k].copy_(xh, non_blocking=True)
+                self.ev_up[k].record(self.up)
+            comp.wait_event(self.ev_up[k])
+            comp.wait_event(self.ev_down[k])          # download i-2 done with y[k]
+            self.step(self.x[k], self.y[k])
+            self.ev_done[k].record(comp)
+            self.ev_free[k].record(comp)
+            with torch.cuda.stream(self.down):
+                self.down.wait_event(self.ev_done[k])
+                yh.copy_(self.y[k], non_blocking=True)
+                self.ev_down[k].record(self.down)
+        comp.wait_stream(self.down)
+        return ys_host
 
 
 del FlopCounter

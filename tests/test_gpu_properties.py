@@ -307,3 +307,21 @@ def test_slab_interior_boundary_split_equals_slab_apply(cuda, p, kind):
     op_on(cut, hi).apply_device(x[b0:], y[b0:], accumulate=True)
     err = float(torch.linalg.vector_norm(y - y_ref) / torch.linalg.vector_norm(y_ref))
     assert err <= 1e-13
+
+
+def test_host_pipeline_matches_sequential_applies(cuda):
+    """Overlapped host transfers (copy streams) give the same results as
+    one apply after another."""
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    prob = workloads.make_problem(3, 4, 8, 3, seed=5)
+    op = matfree.MatrixFreeOperator(prob)
+    n = prob.shape[1]
+    xs = [torch.randn(n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    ys = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    pipe = matfree.HostPipeline(lambda x, y: op.apply_device(x, y), n, n)
+    pipe.run(xs, ys)
+    torch.cuda.synchronize()
+    for xh, yh in zip(xs, ys):
+        ref = op.apply_device(xh.cuda()).cpu()
+        assert torch.equal(yh, ref)
