@@ -212,7 +212,7 @@ class AssemblyProblem:
         tabs = self._cache.get("trial_tables")
         if tabs is None:
             md = max(max(t) for t in self.theta_set)
-            tabs = tuple(tabulate(b, r.points, min(md, b.order - 1)) for b, r in zip(self.trial, self.quad.rules))
+            tabs = tuple(_tabulate(b, r.points, min(md, b.order - 1)) for b, r in zip(self.trial, self.quad.rules))
             self._cache["trial_tables"] = tabs
         return tabs
 
@@ -223,7 +223,7 @@ class AssemblyProblem:
                 tabs = self.trial_tables()
             else:
                 md = max(max(t) for t in self.eta_set)
-                tabs = tuple(tabulate(b, r.points, min(md, b.order - 1)) for b, r in zip(self.test, self.quad.rules))
+                tabs = tuple(_tabulate(b, r.points, min(md, b.order - 1)) for b, r in zip(self.test, self.quad.rules))
             self._cache["test_tables"] = tabs
         return tabs
 
@@ -248,6 +248,13 @@ class AssemblyProblem:
                                  slab=slab)
             self._cache[key] = hit
         return hit
+
+
+def _tabulate(basis, points, max_deriv):
+    # restricted bases (localized.RestrictedBasis) tabulate through their parent
+    if hasattr(basis, "tabulate"):
+        return basis.tabulate(points, max_deriv)
+    return tabulate(basis, points, max_deriv)
 
 
 def _check_block_indices(problem, theta, eta):
