@@ -2,9 +2,9 @@
 
 A drop-in for the hot path of the reference package `igasum`
 (arXiv:1809.05471): the same module names, classes and call signatures
-(bspline, quadrature, tensorspace, geometry.CoefficientField, sumfac,
-matfree), with every computation on the path executed by hand-written
-sm_100a CUDA kernels in libigs_b200.so behind a C-ABI (include/igs_capi.h).
+(bspline, quadrature, tensorspace, geometry, sumfac, matfree, localized),
+with every computation on the path executed by hand-written sm_100a CUDA
+kernels in libigs_b200.so behind a C-ABI (include/igs_capi.h).
 """
 
 from . import errors
@@ -20,6 +20,6 @@ def __getattr__(name):
     import importlib
 
     if name in ("bspline", "quadrature", "tensorspace", "geometry", "sumfac", "matfree",
-                "sharded", "workloads", "build", "_lib"):
+                "localized", "solvers", "sharded", "workloads", "build", "_lib"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)
