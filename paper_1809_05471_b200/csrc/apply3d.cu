@@ -123,7 +123,7 @@ struct ApplyArgs {
 // fp64 tensor-core MMA (DMMA.8x8x4 on sm_100a): D(8x8) += A(8x4) · B(4x8).
 // Fragments (lane = 4·g + m): A[g][m], B[m][g], D[g][2m], D[g][2m+1].
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -538,8 +538,21 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
               cn[2][s] = STIFF ? Crow[2 * CQL + c1 + m + 4 * s] : 0.0;
             }
           }
+          // forward: U^T[line][pt] = Σ_c C^T[line][c0 + c] · B^T[c][pt].  A
+          // lane's two D values (points 2m, 2m+1) are its A-fragment columns
+          // of the two k-chunks of the transposed product below (no shuffles).
+          double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (MASS) dmma(u[0], u[1], cf[0][s], fb0[s]);
+            if (STIFF) {
+              dmma(ux[0], ux[1], cf[0][s], fb1[s]);
+              dmma(uy[0], uy[1], cf[1][s], fb0[s]);
+              dmma(uz[0], uz[1], cf[2][s], fb0[s]);
+            }
+          }
           // coefficients of (window w, these 8 lines, point layer q2): wait
-          // for the TMA box first so its shared-memory reads overlap the MMAs
+          // for the TMA box after issuing the forward MMAs (they do not need it)
 #ifdef IGS_PHASE_TIMING
           long long tw0_ = clock64();
 #endif
@@ -567,19 +580,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
             ld2(p01, fv[4]);
             ld2(p02, fv[5]);
             ld2(p12, fv[6]);
-          }
-          // forward: U^T[line][pt] = Σ_c C^T[line][c0 + c] · B^T[c][pt].  A
-          // lane's two D values (points 2m, 2m+1) are its A-fragment columns
-          // of the two k-chunks of the transposed product below (no shuffles).
-          double u[2] = {0.0, 0.0}, ux[2] = {0.0, 0.0}, uy[2] = {0.0, 0.0}, uz[2] = {0.0, 0.0};
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            if (MASS) dmma(u[0], u[1], cf[0][s], fb0[s]);
-            if (STIFF) {
-              dmma(ux[0], ux[1], cf[0][s], fb1[s]);
-              dmma(uy[0], uy[1], cf[1][s], fb0[s]);
-              dmma(uz[0], uz[1], cf[2][s], fb0[s]);
-            }
           }
           // pointwise (the x weight is zero past the mesh)
           double g0[2], gx[2], gy[2], gz[2];

@@ -12,7 +12,7 @@ namespace dev {
 // D(8x8) += A(8x4)·B(4x8), fp64 (DMMA.8x8x4).  lane = 4g + m holds A[g][m],
 // B[m][g], D[g][2m], D[g][2m+1].
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
