@@ -12,7 +12,8 @@ import os
 from .errors import CapacityError, DomainError, UnsupportedDerivativeError
 
 _PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG_DIR, "libigs_b200.so")
+# IGS_LIB_PATH: development A/B timing of two builds (tools/ab_time.sh)
+LIB_PATH = os.environ.get("IGS_LIB_PATH") or os.path.join(_PKG_DIR, "libigs_b200.so")
 
 MAX_DIM = 3
 MAX_DERIV_SET = 8
