@@ -259,6 +259,17 @@ __host__ __device__ constexpr void slot_tile_ksteps(int st, int kmax, int& k_lo,
   k_lo = (r_lo * Q) / 4;
   k_hi = ((r_hi + P) * Q + 3) / 4 < kmax ? ((r_hi + P) * Q + 3) / 4 : kmax;
 }
+// shortest k-step range over the slot tiles (equal to the longest: no predicates)
+template <int P, int Q, int T>
+constexpr int min_ksteps(int ntiles, int kmax) {
+  int m = 1 << 30;
+  for (int st = 0; st < ntiles; ++st) {
+    int lo = 0, hi = 0;
+    slot_tile_ksteps<P, Q, T>(st, kmax, lo, hi);
+    if (hi - lo < m) m = hi - lo;
+  }
+  return m;
+}
 // longest k-step range over the slot tiles (static unroll bound)
 template <int P, int Q, int T>
 constexpr int max_ksteps(int ntiles, int kmax) {
@@ -286,6 +297,8 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int PT = C::PT, PTP = C::PTP, XR = C::XR, XRP = C::XRP, XK = C::XK;
   constexpr int NT = C::NT, NW = C::NW, SP = C::SP, YP = C::YP, W = C::W;
   constexpr int KL1 = max_ksteps<P, Q, T>(PTP / 8, XK / 4), KL2 = max_ksteps<P, Q, T>(PTP / 8, XRP / 4);
+  constexpr bool kFullK1 = KL1 == min_ksteps<P, Q, T>(PTP / 8, XK / 4);
+  constexpr bool kFullK2 = KL2 == min_ksteps<P, Q, T>(PTP / 8, XRP / 4);
   extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
   const int ng = pl.ng, nh = pl.nh;
@@ -339,7 +352,7 @@ __global__ void __launch_bounds__(512, 1)
         const double* Wb = Wk + pl.b_v0[b] * (XK * SP);
 #pragma unroll
         for (int kk = 0; kk < KL1; ++kk)
-          if (k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
+          if (kFullK1 || k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
         if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
           double* Gd = Gs + (pl.b_g[b] * XRP + y) * SP + st * 8 + 2 * m4;
           Gd[0] = d0;
@@ -383,7 +396,7 @@ __global__ void __launch_bounds__(512, 1)
         const double* Gg = Gk + g * (XRP * SP);
 #pragma unroll
         for (int kk = 0; kk < KL2; ++kk)
-          if (k_lo + kk < k_hi) dmma_a(d0, d1, Wg[kk * 4], Gg[kk * 4 * SP]);
+          if (kFullK2 || k_lo + kk < k_hi) dmma_a(d0, d1, Wg[kk * 4], Gg[kk * 4 * SP]);
         if (g + 1 == pl.ng || pl.g_h[g + 1] != pl.g_h[g]) {
           const int hoff = pl.g_h[g] * kSweepBlock;
           if (ok0) a.H[off0 + hoff] = d0;

@@ -36,10 +36,11 @@ def time_apply(name, K=None, reps=10, generic=False):
           f"B_alg {balg / 1e9:.2f} GB -> {balg / ms / 1e6:.0f} GB/s (setup {setup:.1f}s)", flush=True)
 
 
-def time_assemble(name, K=None, reps=3):
+def time_assemble(name, K=None, reps=10):
     c = workloads.CONFIGS[name]
     prob = workloads.make_problem(c["d"], c["p"], K or c["K"], c["kind"])
-    A = sumfac.assemble(prob)
+    for _ in range(3):
+        A = sumfac.assemble(prob)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
