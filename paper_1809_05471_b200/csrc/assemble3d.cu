@@ -426,15 +426,21 @@ struct Asm3bArgs {
   int grp_v[4];                   // their variant codes in the swept direction
 };
 
-// W^{v(h)}[jn][jm] of the swept (last) direction at the Q points of every
-// element, laid out [e][q][jm][jn][h(4)] (zero for h >= ngrp): the last
-// stage's weights, computed once.
+// Per element record of the swept (last) direction, computed once:
+// W^{v(h)}[jn][jm] at the Q points, [q][jm][jn][h(4)] (zero for h >= ngrp),
+// then the CSR metadata of row m2 = e (row start, width, first column).
 template <int P, int Q, int D>
 __global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
-  constexpr int NWT = Q * P * P * 4, L = D - 1;
+  constexpr int NWT = Q * P * P * 4, NWR = NWT + 4, L = D - 1;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)a.tab.K[L] * NWT) return;
-  const int e2 = (int)(i / NWT), r = (int)(i % NWT);
+  if (i >= (int64_t)a.tab.K[L] * NWR) return;
+  const int e2 = (int)(i / NWR), r = (int)(i % NWR);
+  if (r >= NWT) {  // row metadata of row m2 = e2: CSR row start, width, first column
+    const int64_t rp2 = a.pat.rp[L][e2];
+    const int64_t v = r == NWT ? rp2 : r == NWT + 1 ? a.pat.rp[L][e2 + 1] - rp2 : r == NWT + 2 ? a.pat.cl[L][rp2] : 0;
+    reinterpret_cast<int64_t*>(w2g)[i] = v;
+    return;
+  }
   const int hh = r % 4, jn = (r / 4) % P, jm = (r / (4 * P)) % P, q = r / (4 * P * P);
   double val = 0.0;
   if (hh < a.ngrp) {
@@ -448,7 +454,6 @@ __global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
   w2g[i] = val;
 }
 
-
 // Last-direction pipeline: shared-memory ring of NS3 element stages, each
 // filled by two bulk copies (the block's H tile and the element weights)
 // D3 = NS3 - 2 elements ahead.
@@ -456,8 +461,9 @@ constexpr int NS3 = 4, D3 = NS3 - 2, NT3 = kSweepBlock;
 template <int P, int Q>
 struct S3Cfg {
   static constexpr int NWT = Q * P * P * 4;   // weights per element
+  static constexpr int NWR = NWT + 4;         // + row metadata (3 int64, padded)
   static constexpr int HST = Q * 4 * NT3;     // H values per stage [q][group <= 4][thread]
-  static constexpr size_t SMEM = (size_t)NS3 * (HST + NWT) * sizeof(double) + NS3 * sizeof(uint64_t);
+  static constexpr size_t SMEM = (size_t)NS3 * (HST + NWR) * sizeof(double) + NS3 * sizeof(uint64_t);
 };
 
 // Last-direction sweep (3D stage 3, 2D stage 2).  Block = (chunk of
@@ -472,12 +478,12 @@ struct S3Cfg {
 template <int P, int Q, int D>
 __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs a) {
   using C = S3Cfg<P, Q>;
-  constexpr int W = 2 * P - 1, NWT = C::NWT, L = D - 1;
+  constexpr int W = 2 * P - 1, NWT = C::NWT, NWR = C::NWR, L = D - 1;
   static_assert(NWT % 2 == 0, "16-byte table chunks");
   extern __shared__ __align__(16) double s3[];
   double* hst = s3;                    // [NS3][Q][ngrp][NT3]
-  double* w2s = s3 + NS3 * C::HST;     // [NS3][Q][P][P][4]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWT);
+  double* w2s = s3 + NS3 * C::HST;     // [NS3][NWR]: weights [Q][P][P][4] + row metadata
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWR);
   const int nh = a.ngrp;
   const int tid = threadIdx.x;
   const int64_t npairs = a.NS0 * a.NS1;
@@ -514,14 +520,15 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
   const int c_lo = a.e_lo + chunk_id * a.chunk;
   const int c_hi = min(a.e_hi, c_lo + a.chunk);
   const int e_lo = max(a.e_lo, c_lo - (P - 1)), e_hi = c_hi;
-  auto flush = [&](int64_t m2, const double* row) {
+  const int64_t base = *a.base;
+  // meta = {rp2, w2, lo2} of row m2 (from the element record in shared
+  // memory, or from the pattern for the trailing rows)
+  auto flush = [&](int64_t m2, const double* row, const int64_t* meta) {
     if (m2 < c_lo || (m2 >= c_hi && c_hi != K2)) return;
-    const int64_t rp2 = a.pat.rp[L][m2];
-    const int64_t w2 = a.pat.rp[L][m2 + 1] - rp2;
-    const int64_t lo2 = a.pat.cl[L][rp2];
+    const int64_t rp2 = meta[0], w2 = meta[1], lo2 = meta[2];
     const int64_t m = m0 + N0 * (m1 + N1 * m2);
     if (m < a.row_lo || m >= a.row_hi) return;
-    const int64_t start = rp0 * w1 * w2 + P0 * rp1 * w2 + P0 * P1 * rp2 - *a.base;
+    const int64_t start = rp0 * w1 * w2 + P0 * rp1 * w2 + P0 * P1 * rp2 - base;
 #pragma unroll
     for (int k = 0; k < W; ++k) {
       const int64_t n2 = m2 + k - (P - 1);
@@ -529,14 +536,14 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
     }
   };
   const unsigned htile = (unsigned)(Q * nh * NT3 * sizeof(double));
-  const unsigned wbytes = (unsigned)(NWT * sizeof(double));
+  const unsigned wbytes = (unsigned)(NWR * sizeof(double));
   const double* hblock = a.H + sb * a.NE * Q * nh * NT3;
   auto issue = [&](int e2) {  // one thread
     if (e2 >= e_hi) return;
     const int stg = (e2 - e_lo) % NS3;
     dev::mbar_expect_tx(bars + stg, htile + wbytes);
     dev::bulk_load(hst + stg * C::HST, hblock + (int64_t)(e2 - a.e_lo) * Q * nh * NT3, htile, bars + stg);
-    dev::bulk_load(w2s + stg * NWT, a.w2g + (int64_t)e2 * NWT, wbytes, bars + stg);
+    dev::bulk_load(w2s + stg * NWR, a.w2g + (int64_t)e2 * NWR, wbytes, bars + stg);
   };
   if (tid < NS3) dev::mbar_init(bars + tid, 1);
   dev::fence_mbar_init();
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       const int stg = (e2 - e_lo) % NS3;
       dev::mbar_wait(bars + stg, (unsigned)(((e2 - e_lo) / NS3) & 1));
       const double* hcol = hst + stg * C::HST + tid;
-      const double* wst = w2s + stg * NWT;
+      const double* wst = w2s + stg * NWR;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const double h0 = hcol[(q * nh + 0) * NT3];
@@ -580,7 +587,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
           }
       }
       // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
-      if (valid) flush(e2, ring[r]);
+      if (valid) flush(e2, ring[r], reinterpret_cast<const int64_t*>(wst + NWT));
 #pragma unroll
       for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
     }
@@ -592,8 +599,11 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       const int64_t m2 = K2 - 1 + t;
       const int slot = (int)((m2 - e_lo) % P);
 #pragma unroll
+      const int64_t rp2 = a.pat.rp[L][m2];
+      const int64_t meta[3] = {rp2, a.pat.rp[L][m2 + 1] - rp2, a.pat.cl[L][rp2]};
+#pragma unroll
       for (int s = 0; s < P; ++s)
-        if (s == slot) flush(m2, ring[s]);
+        if (s == slot) flush(m2, ring[s], meta);
     }
   }
 }
@@ -809,10 +819,10 @@ size_t asm_workspace(const AsmShape& s) {
   auto padded = [](int64_t n) { return (size_t)ceil_div(n, (int64_t)kSweepBlock) * kSweepBlock; };
   if (s.fs.d == 3) {
     return padded((s.fs.nfn[1] * W) * (s.fs.nfn[0] * W)) * s.zpts * s.plan.nh * sizeof(double) +
-           (size_t)s.fs.nel[2] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
+           (size_t)s.fs.nel[2] * (s.fs.k * s.fs.p * s.fs.p * 4 + 4) * sizeof(double) + 512;
   }
   return padded(s.fs.nfn[0] * W) * s.fs.npt[1] * s.plan.ng * sizeof(double) +
-         (size_t)s.fs.nel[1] * s.fs.k * s.fs.p * s.fs.p * 4 * sizeof(double) + 512;
+         (size_t)s.fs.nel[1] * (s.fs.k * s.fs.p * s.fs.p * 4 + 4) * sizeof(double) + 512;
 }
 
 // z elements the row range needs (rows of DoF layers [m2a, m2b] are summed
@@ -918,7 +928,7 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.ngrp = s.plan.nh;
   for (int h = 0; h < 4; ++h) b.grp_v[h] = h < s.plan.nh ? s.plan.h_v2[h] : 0;
   {
-    const int64_t n = (int64_t)tab.K[2] * Q * P * P * 4;
+    const int64_t n = (int64_t)tab.K[2] * S3Cfg<P, Q>::NWR;
     asm_wlast_kernel<P, Q, 3><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);
     IGS_LAUNCH_CHECK("asm_wlast_kernel");
   }
@@ -1008,7 +1018,7 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.ngrp = s.plan.ng;
   for (int g = 0; g < 4; ++g) b.grp_v[g] = g < s.plan.ng ? s.plan.g_v1[g] : 0;
   {
-    const int64_t n = (int64_t)K1 * Q * P * P * 4;
+    const int64_t n = (int64_t)K1 * S3Cfg<P, Q>::NWR;
     asm_wlast_kernel<P, Q, 2><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, wlg);
     IGS_LAUNCH_CHECK("asm_wlast_kernel");
   }
