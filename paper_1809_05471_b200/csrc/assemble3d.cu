@@ -22,6 +22,7 @@
 //         ring[m2][n2] += Σ_h W_z^{v2(h)} H_h  ->  CSR
 //   2D: asm2_stage1 (x) -> HBM, asm_sweep<2> (y ring, chunked) -> CSR.
 #include "fused.cuh"
+#include <cstdlib>
 #include "tma.cuh"
 
 namespace igs {
@@ -45,6 +46,8 @@ struct AsmPlan {
   int b_ps[kMaxBlocks];         // block -> index into pl_list
   int g_b0[kMaxBlocks], g_nb[kMaxBlocks];  // blocks of group g: [g_b0, g_b0 + g_nb)
   int h_g0[kMaxBlocks], h_ng[kMaxBlocks];  // groups of stage-2 group h (3D)
+  int half_b;                   // 3D stage 1: blocks [0, half_b) | [half_b, nb), whole
+                                // groups, balanced by block count
 };
 
 bool build_plan(const igs_problem* p, AsmPlan* plan) {
@@ -126,6 +129,19 @@ bool build_plan(const igs_problem* p, AsmPlan* plan) {
         ++nbo;
       }
     Q.g_nb[gn] = nbo - Q.g_b0[gn];
+  }
+  // two contiguous group ranges with ~nb/2 blocks each (stage-1 warp halves)
+  Q.half_b = Q.nb;
+  {
+    int best = 1 << 30;
+    for (int gn = 0; gn < Q.ng; ++gn) {
+      const int end = Q.g_b0[gn] + Q.g_nb[gn];
+      const int imb = std::abs(2 * end - Q.nb);
+      if (end < Q.nb && imb < best) {
+        best = imb;
+        Q.half_b = end;
+      }
+    }
   }
   *plan = Q;
   return true;
@@ -298,6 +314,7 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int NT = C::NT, NW = C::NW, SP = C::SP, YP = C::YP, W = C::W;
   constexpr int KL1 = max_ksteps<P, Q, T>(PTP / 8, XK / 4), KL2 = max_ksteps<P, Q, T>(PTP / 8, XRP / 4);
   constexpr bool kFullK1 = KL1 == min_ksteps<P, Q, T>(PTP / 8, XK / 4);
+  constexpr int NYP = (XRP / 8 + 1) / 2;  // pairs of y tiles
   constexpr bool kFullK2 = KL2 == min_ksteps<P, Q, T>(PTP / 8, XRP / 4);
   extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
@@ -333,31 +350,44 @@ __global__ void __launch_bounds__(512, 1)
   unsigned phase = 0;
   for (int64_t x2 = z_lo; x2 < z_hi; ++x2, phase ^= 1) {
     dev::mbar_wait(bar, phase);
-    // ---- stage 1: task = (y tile, s0 tile), all groups --------------------------
-    // blocks are ordered by group: the accumulator is stored and reset after
-    // the last block of each group (static block index: plan reads are
-    // constant-bank immediates)
-    for (int t = warp; t < (XRP / 8) * (PTP / 8); t += NW) {
-      const int yt = t / (PTP / 8), st = t % (PTP / 8);
+    // ---- stage 1: task = (pair of y tiles, s0 tile, half of the blocks) --------
+    // Both y tiles share every W0 fragment (shared-memory traffic is the
+    // stage's bound); the block halves are whole groups.  Blocks are ordered
+    // by group: the accumulators are stored and reset after a group's last
+    // block (static block index: plan reads are constant-bank immediates).
+    for (int t = warp; t < NYP * (PTP / 8) * 2; t += NW) {
+      const int half = t & 1, st = (t >> 1) % (PTP / 8), yp = (t >> 1) / (PTP / 8);
       int k_lo, k_hi;
       slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
-      const int y = yt * 8 + g8;
-      const double* Fy = Fs + y * XR + m4 + k_lo * 4;
+      const bool y1ok = 2 * yp + 1 < XRP / 8;
+      const int y0 = 2 * yp * 8 + g8, y1 = y1ok ? y0 + 8 : y0;
+      const double* F0 = Fs + y0 * XR + m4 + k_lo * 4;
+      const double* F1 = Fs + y1 * XR + m4 + k_lo * 4;
       const double* Wk = W0 + (m4 + k_lo * 4) * SP + st * 8 + g8;
-      double d0 = 0.0, d1 = 0.0;
+      const int b_lo = half ? pl.half_b : 0, b_hi = half ? pl.nb : pl.half_b;
+      double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
 #pragma unroll
       for (int b = 0; b < kMaxBlocks; ++b) {
-        if (b >= pl.nb) break;
-        const double* Fb = Fy + pl.b_plane[b] * (XRP * XR);
+        if (b < b_lo) continue;
+        if (b >= b_hi) break;
+        const int po = pl.b_plane[b] * (XRP * XR);
         const double* Wb = Wk + pl.b_v0[b] * (XK * SP);
 #pragma unroll
         for (int kk = 0; kk < KL1; ++kk)
-          if (kFullK1 || k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
+          if (kFullK1 || k_lo + kk < k_hi) {
+            const double w = Wb[kk * 4 * SP];
+            dmma_a(c0[0], c0[1], F0[po + kk * 4], w);
+            dmma_a(c1[0], c1[1], F1[po + kk * 4], w);
+          }
         if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
-          double* Gd = Gs + (pl.b_g[b] * XRP + y) * SP + st * 8 + 2 * m4;
-          Gd[0] = d0;
-          Gd[1] = d1;
-          d0 = d1 = 0.0;
+          double* Gd = Gs + (pl.b_g[b] * XRP + y0) * SP + st * 8 + 2 * m4;
+          Gd[0] = c0[0];
+          Gd[1] = c0[1];
+          if (y1ok) {
+            Gd[8 * SP] = c1[0];
+            Gd[8 * SP + 1] = c1[1];
+          }
+          c0[0] = c0[1] = c1[0] = c1[1] = 0.0;
         }
       }
     }
