@@ -381,12 +381,8 @@ __global__ void __launch_bounds__(512, 1)
           }
         if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
           double* Gd = Gs + (pl.b_g[b] * XRP + y0) * SP + st * 8 + 2 * m4;
-          Gd[0] = c0[0];
-          Gd[1] = c0[1];
-          if (y1ok) {
-            Gd[8 * SP] = c1[0];
-            Gd[8 * SP + 1] = c1[1];
-          }
+          *reinterpret_cast<double2*>(Gd) = make_double2(c0[0], c0[1]);
+          if (y1ok) *reinterpret_cast<double2*>(Gd + 8 * SP) = make_double2(c1[0], c1[1]);
           c0[0] = c0[1] = c1[0] = c1[1] = 0.0;
         }
       }
@@ -453,15 +449,16 @@ struct Asm3bArgs {
   int64_t NE;                     // elements held by H (sweep-blocked layout)
   int chunk;                      // elements per thread chunk (rows written per chunk)
   int ngrp;                       // groups summed per point (3D: nh, 2D: ng)
-  int grp_v[4];                   // their variant codes in the swept direction
+  int vmap[4];                    // group holding variant v = θ + 2η of the swept direction (-1: none)
 };
 
-// Per element record of the swept (last) direction, computed once:
-// W^{v(h)}[jn][jm] at the Q points, [q][jm][jn][h(4)] (zero for h >= ngrp),
-// then the CSR metadata of row m2 = e (row start, width, first column).
+// Per element record of the swept (last) direction, computed once: the
+// separable factors of W^{θ+2η}[jn][jm](q) = (w·B^θ_jn)(q) · B^η_jm(q),
+// [q][wB^0 | wB^1 | B^0 | B^1][P padded to even], then the CSR metadata of row m2 = e (row
+// start, width, first column).
 template <int P, int Q, int D>
 __global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
-  constexpr int NWT = Q * P * P * 4, NWR = NWT + 4, L = D - 1;
+  constexpr int PP = (P + 1) & ~1, NWT = Q * 4 * PP, NWR = NWT + 4, L = D - 1;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)a.tab.K[L] * NWR) return;
   const int e2 = (int)(i / NWR), r = (int)(i % NWR);
@@ -471,17 +468,15 @@ __global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
     reinterpret_cast<int64_t*>(w2g)[i] = v;
     return;
   }
-  const int hh = r % 4, jn = (r / 4) % P, jm = (r / (4 * P)) % P, q = r / (4 * P * P);
-  double val = 0.0;
-  if (hh < a.ngrp) {
-    const int v = a.grp_v[hh];
-    const int64_t x = (int64_t)e2 * Q + q;
-    const double w = a.tab.wts[L][x];
-    const double bn = (v & 1) > a.tab.md[L] ? 0.0 : a.tab.vals[L][((int64_t)(v & 1) * P + jn) * a.tab.X[L] + x];
-    const double bm = (v >> 1) > a.tab.md[L] ? 0.0 : a.tab.vals[L][((int64_t)(v >> 1) * P + jm) * a.tab.X[L] + x];
-    val = (w * bn) * bm;
+  const int j = r % PP, f = (r / PP) % 4, q = r / (4 * PP);
+  const int lvl = f & 1;
+  if (j >= P) {
+    w2g[i] = 0.0;
+    return;
   }
-  w2g[i] = val;
+  const int64_t x = (int64_t)e2 * Q + q;
+  const double b = lvl > a.tab.md[L] ? 0.0 : a.tab.vals[L][((int64_t)lvl * P + j) * a.tab.X[L] + x];
+  w2g[i] = f < 2 ? a.tab.wts[L][x] * b : b;
 }
 
 // Last-direction pipeline: shared-memory ring of NS3 element stages, each
@@ -490,7 +485,8 @@ __global__ void asm_wlast_kernel(const Asm3bArgs a, double* w2g) {
 constexpr int NS3 = 4, D3 = NS3 - 2, NT3 = kSweepBlock;
 template <int P, int Q>
 struct S3Cfg {
-  static constexpr int NWT = Q * P * P * 4;   // weights per element
+  static constexpr int PP = (P + 1) & ~1;     // factor row pitch (16-byte rows)
+  static constexpr int NWT = Q * 4 * PP;      // separable weight factors per element
   static constexpr int NWR = NWT + 4;         // + row metadata (3 int64, padded)
   static constexpr int HST = Q * 4 * NT3;     // H values per stage [q][group <= 4][thread]
   static constexpr size_t SMEM = (size_t)NS3 * (HST + NWR) * sizeof(double) + NS3 * sizeof(uint64_t);
@@ -508,11 +504,11 @@ struct S3Cfg {
 template <int P, int Q, int D>
 __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs a) {
   using C = S3Cfg<P, Q>;
-  constexpr int W = 2 * P - 1, NWT = C::NWT, NWR = C::NWR, L = D - 1;
+  constexpr int W = 2 * P - 1, NWT = C::NWT, NWR = C::NWR, PP = C::PP, L = D - 1;
   static_assert(NWT % 2 == 0, "16-byte table chunks");
   extern __shared__ __align__(16) double s3[];
   double* hst = s3;                    // [NS3][Q][ngrp][NT3]
-  double* w2s = s3 + NS3 * C::HST;     // [NS3][NWR]: weights [Q][P][P][4] + row metadata
+  double* w2s = s3 + NS3 * C::HST;     // [NS3][NWR]: factors [Q][4][P] + row metadata
   uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWR);
   const int nh = a.ngrp;
   const int tid = threadIdx.x;
@@ -596,24 +592,38 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       dev::mbar_wait(bars + stg, (unsigned)(((e2 - e_lo) / NS3) & 1));
       const double* hcol = hst + stg * C::HST + tid;
       const double* wst = w2s + stg * NWR;
+      // Σ_{θ,η} (wB^θ_jn)(B^η_jm) H_{θ+2η}: contract θ first (u_η[jn]),
+      // then η into the ring (P·P·2 + 4P FMAs, 4P broadcast factors per q)
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const double h0 = hcol[(q * nh + 0) * NT3];
-        const double h1 = nh > 1 ? hcol[(q * nh + 1) * NT3] : 0.0;
-        const double h2 = nh > 2 ? hcol[(q * nh + 2) * NT3] : 0.0;
-        const double h3 = nh > 3 ? hcol[(q * nh + 3) * NT3] : 0.0;
+        double hv[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) hv[v] = a.vmap[v] >= 0 ? hcol[(q * nh + a.vmap[v]) * NT3] : 0.0;
+        double fb[4][P];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int j = 0; j < P; j += 2) {
+            if (j + 1 < P) {
+              const double2 t = *reinterpret_cast<const double2*>(wst + (q * 4 + f) * PP + j);
+              fb[f][j] = t.x;
+              fb[f][j + 1] = t.y;
+            } else {
+              fb[f][j] = wst[(q * 4 + f) * PP + j];
+            }
+          }
+        double u0[P], u1[P];
+#pragma unroll
+        for (int jn = 0; jn < P; ++jn) {
+          u0[jn] = fma(fb[1][jn], hv[1], fb[0][jn] * hv[0]);
+          u1[jn] = fma(fb[1][jn], hv[3], fb[0][jn] * hv[2]);
+        }
 #pragma unroll
         for (int jm = 0; jm < P; ++jm)
 #pragma unroll
           for (int jn = 0; jn < P; ++jn) {
-            const double2 wa = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4);
-            const double2 wb = *reinterpret_cast<const double2*>(wst + ((q * P + jm) * P + jn) * 4 + 2);
-            double sacc = ring[(r + jm) % P][jn - jm + P - 1];
-            sacc = fma(wa.x, h0, sacc);
-            sacc = fma(wa.y, h1, sacc);
-            sacc = fma(wb.x, h2, sacc);
-            sacc = fma(wb.y, h3, sacc);
-            ring[(r + jm) % P][jn - jm + P - 1] = sacc;
+            double& acc = ring[(r + jm) % P][jn - jm + P - 1];
+            acc = fma(fb[3][jm], u1[jn], fma(fb[2][jm], u0[jn], acc));
           }
       }
       // row m2 = e2 is final: write its 2P-1 columns, recycle the ring row
@@ -849,10 +859,10 @@ size_t asm_workspace(const AsmShape& s) {
   auto padded = [](int64_t n) { return (size_t)ceil_div(n, (int64_t)kSweepBlock) * kSweepBlock; };
   if (s.fs.d == 3) {
     return padded((s.fs.nfn[1] * W) * (s.fs.nfn[0] * W)) * s.zpts * s.plan.nh * sizeof(double) +
-           (size_t)s.fs.nel[2] * (s.fs.k * s.fs.p * s.fs.p * 4 + 4) * sizeof(double) + 512;
+           (size_t)s.fs.nel[2] * (s.fs.k * 4 * (s.fs.p + 1) + 4) * sizeof(double) + 512;
   }
   return padded(s.fs.nfn[0] * W) * s.fs.npt[1] * s.plan.ng * sizeof(double) +
-         (size_t)s.fs.nel[1] * (s.fs.k * s.fs.p * s.fs.p * 4 + 4) * sizeof(double) + 512;
+         (size_t)s.fs.nel[1] * (s.fs.k * 4 * (s.fs.p + 1) + 4) * sizeof(double) + 512;
 }
 
 // z elements the row range needs (rows of DoF layers [m2a, m2b] are summed
@@ -956,7 +966,8 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.e_hi = z.e_hi;
   b.chunk = z.e_hi - z.e_lo;
   b.ngrp = s.plan.nh;
-  for (int h = 0; h < 4; ++h) b.grp_v[h] = h < s.plan.nh ? s.plan.h_v2[h] : 0;
+  for (int v = 0; v < 4; ++v) b.vmap[v] = -1;
+  for (int h = 0; h < s.plan.nh; ++h) b.vmap[s.plan.h_v2[h]] = h;
   {
     const int64_t n = (int64_t)tab.K[2] * S3Cfg<P, Q>::NWR;
     asm_wlast_kernel<P, Q, 3><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w2g);
@@ -1046,7 +1057,8 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.chunk = chunk;
   if (s.plan.ng > 4) return fail(IGS_ECAPACITY, "2D fused assembly sums at most 4 variant groups");
   b.ngrp = s.plan.ng;
-  for (int g = 0; g < 4; ++g) b.grp_v[g] = g < s.plan.ng ? s.plan.g_v1[g] : 0;
+  for (int v = 0; v < 4; ++v) b.vmap[v] = -1;
+  for (int g = 0; g < s.plan.ng; ++g) b.vmap[s.plan.g_v1[g]] = g;
   {
     const int64_t n = (int64_t)K1 * S3Cfg<P, Q>::NWR;
     asm_wlast_kernel<P, Q, 2><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, wlg);
