@@ -160,6 +160,22 @@ igs_status igs_assemble_values(const igs_problem* prob, const int64_t* const* ro
                                const double* planes, double* values, void* ws,
                                size_t ws_bytes, int32_t flags, void* stream);
 
+/* ---- a22: direct-quadrature comparison oracle ------------------------- */
+/* assemble_naive (sumfac.py:388-477) on the device: every entry of rows
+ * [row_lo, row_hi) — entries [entry_lo, entry_hi) = indptr[row_lo],
+ * indptr[row_hi] (host copies) — sums the weighted integrand of every
+ * non-zero (theta, eta) block over the box where the knot supports of its
+ * trial and test functions overlap (_support_column_ranges :382-385), with
+ * no W operators or intermediates: an independent check of K3.  values
+ * [entry_hi - entry_lo].  `updates` (device uint64 or NULL) is incremented
+ * by the box size of every (entry, block), the reference's block_update
+ * count (:475).  Whole fields only (no slab).  Small sizes: the caller
+ * applies the reference's nominal-work budget. */
+igs_status igs_assemble_naive(const igs_problem* prob, const int64_t* indptr, const void* indices,
+                              int32_t index_bytes, int64_t row_lo, int64_t row_hi, int64_t entry_lo,
+                              int64_t entry_hi, const double* planes, double* values,
+                              uint64_t* updates, void* stream);
+
 /* ---- K4: matrix-free apply (Alg. 2 + Alg. 3) --------- */
 /* y = A x (or y += A x with IGS_FLAG_ACCUMULATE).  x has the trial DoF
  * count, y the test DoF count (of the slab, see igs_problem). */

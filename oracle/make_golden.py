@@ -192,7 +192,37 @@ def golden_geometry():
          indices=A.pattern.indices)
 
 
-if __name__ == "__main__":
+def golden_naive():
+    """The reference's own comparison oracles (sumfac.py:388-509): values and
+    block_update counter of assemble_naive, and assemble_kronecker_dense, on a
+    3D mass+stiffness case and a 2D Petrov-Galerkin case with reduced
+    smoothness, a non-symmetric F and a custom rule in one direction."""
+    prob, planes = ref_problem(3, 3, 3, 3)
+    counter = sumfac.FlopCounter()
+    A = sumfac.assemble_naive(prob, counter)
+    save("naive_d3_p3", meta=np.array([3, 3, 3, 3]), values=A.values, counter=np.array(counter.as_tuple()),
+         indptr=prob.pattern().indptr, indices=prob.pattern().indices)
+    tk = [bspline.uniform_open_knots(3, 4, interior_multiplicity=2), bspline.uniform_open_knots(3, 3)]
+    sk = [bspline.uniform_open_knots(2, 4), bspline.uniform_open_knots(2, 3)]
+    rules = [quadrature.per_element_rule(np.unique(tk[0].knots), 3),
+             quadrature.custom_rule(np.linspace(0.01, 0.99, 11), np.full(11, 1.0 / 11))]
+    quad = quadrature.TensorQuadrature(rules)
+    theta = [(0, 0), (1, 0), (0, 1)]
+    F = np.random.default_rng(3).uniform(-1, 1, (quad.num_points, 3, 3))
+    field = geometry.CoefficientField(theta, theta, F, quad.shape)
+    prob = sumfac.AssemblyProblem([bspline.UnivariateBasis(k) for k in tk], [bspline.UnivariateBasis(k) for k in sk],
+                                  quad, field)
+    counter = sumfac.FlopCounter()
+    A = sumfac.assemble_naive(prob, counter)
+    D = sumfac.assemble_kronecker_dense(prob)
+    save("naive_d2_pg", F=F, values=A.values, counter=np.array(counter.as_tuple()), dense=D,
+         indptr=prob.pattern().indptr, indices=prob.pattern().indices)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    for name in sys.argv[1:]:
+        globals()["golden_" + name]()
+elif __name__ == "__main__":
     golden_gauss()
     golden_tabulate()
     golden_pattern()
@@ -200,3 +230,4 @@ if __name__ == "__main__":
     golden_apply()
     golden_blocks()
     golden_geometry()
+    golden_naive()

@@ -118,6 +118,10 @@ _SIGNATURES = [
      [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
     ("igs_write_matrix_market", ctypes.c_int,
      [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("igs_assemble_naive", ctypes.c_int,
+     [ctypes.POINTER(IgsProblem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+      ctypes.c_void_p]),
     ("igs_geometry_pullback", ctypes.c_int,
      [ctypes.POINTER(IgsPullbackArgs), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_size_t,

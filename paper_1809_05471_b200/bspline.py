@@ -80,8 +80,7 @@ class KnotVector:
         t = self._dev.get(name)
         if t is None:
             torch = _lib.require_cuda()
-            t = torch.as_tensor(np.ascontiguousarray(getattr(self, name)), dtype=torch.float64,
-                                device="cuda")
+            t = torch.tensor(np.asarray(getattr(self, name), dtype=np.float64), device="cuda")
             self._dev[name] = t
         return t
 

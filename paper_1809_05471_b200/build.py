@@ -35,6 +35,7 @@ SOURCES = [
     "apply3d.cu",
     "assemble3d.cu",
     "geometry.cu",
+    "naive.cu",
     "mmio.cpp",
 ]
 

@@ -27,7 +27,15 @@ __all__ = (
     "assemble",
     "assemble_block",
     "rel_frobenius",
+    "assemble_naive",
+    "assemble_kronecker_dense",
+    "DEFAULT_NAIVE_BUDGET",
+    "DEFAULT_DENSE_BUDGET",
 )
+
+# nominal-work guards of the comparison oracles (sumfac.py:43-44)
+DEFAULT_NAIVE_BUDGET = 4_000_000_000
+DEFAULT_DENSE_BUDGET = 100_000_000
 
 
 class FlopCounter:
@@ -368,5 +376,64 @@ def fused_path(problem, op="assemble", dir_order=None):
     return int(lib.igs_fused_path(ctypes.byref(prob), _lib.OP_ASSEMBLE if op == "assemble" else _lib.OP_APPLY))
 
 
+def _naive_values(problem, counter):
+    torch = _lib.require_cuda()
+    lib = _lib.load()
+    pat = problem.pattern()
+    values = torch.zeros(pat.nnz, dtype=torch.float64, device="cuda")
+    if pat.nnz == 0 or problem.quad.num_points == 0:
+        return values
+    if problem.slab is not None:
+        raise ValueError("the naive oracle takes whole coefficient fields (no slab)")
+    prob, keep = problem.struct(None)
+    f = problem.coeff_field()
+    updates = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st = lib.igs_assemble_naive(ctypes.byref(prob), _lib.ptr(pat.indptr_dev), _lib.ptr(pat.indices_dev),
+                                pat.indices_dev.element_size(), 0, pat.shape[0], 0, pat.nnz,
+                                _lib.ptr(f.planes), _lib.ptr(values), _lib.ptr(updates), _lib.stream_handle())
+    _lib.check(st, "assemble_naive")
+    if counter is not None:
+        counter.add_block_update(int(updates.item()))
+    return values
+
+
+def assemble_naive(problem, counter=None, budget=DEFAULT_NAIVE_BUDGET):
+    """Direct quadrature sum per pattern entry: the comparison oracle
+    (sumfac.py:388-477), one device thread per CSR entry (igs_assemble_naive).
+
+    Same guard as the reference: pattern nnz x points x derivative blocks
+    above `budget` raises CapacityError; the counter gets the reference's
+    block_update count (the support-overlap box of every entry and block).
+    """
+    counter = counter if counter is not None else FlopCounter()
+    pattern = problem.pattern()
+    n_blocks = len(problem.theta_set) * len(problem.eta_set)
+    nominal = pattern.nnz * problem.quad.num_points * n_blocks
+    if nominal > budget:
+        raise CapacityError(f"naive assembly would take {nominal} nominal operations, above {budget}")
+    return SparseMatrix(pattern, _naive_values(problem, counter))
+
+
+def assemble_kronecker_dense(problem, budget=DEFAULT_DENSE_BUDGET):
+    """Dense (test x trial) numpy matrix of the full operator (sumfac.py:480-509).
+
+    The reference materialises Kronecker products of the dense 1D tables;
+    every entry outside the tensor pattern is an exact zero of that product,
+    so the device computes the pattern entries by direct quadrature
+    (igs_assemble_naive) and scatters them into the dense array.
+    """
+    m_total, n_total = problem.shape
+    npts = problem.quad.num_points
+    if m_total * n_total * max(npts, 1) > budget:
+        raise CapacityError("instance too large for the dense Kronecker oracle")
+    out = np.zeros((m_total, n_total))
+    pat = problem.pattern()
+    if pat.nnz == 0:
+        return out
+    vals = _naive_values(problem, None).cpu().numpy()
+    rows = np.repeat(np.arange(m_total), np.diff(pat.indptr))
+    out[rows, pat.indices] = vals
+    return out
+
+
 __all__ += ("block_update_count", "fused_path")
-del CapacityError
