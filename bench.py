@@ -416,7 +416,9 @@ def main():
                          "kernel": "apply3d_kernel", "kernel_ms": k_ms, "alg_bytes_per_launch": b_alg},
             "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * n_own,
                     "d2h_bytes_per_step": 8 * n_own},
-            "gpu_launches": args.steps * (2 if world == 1 else 2),
+            # per step: apply3d + reduce; rank 0 of a slab run: x copy, interior
+            # and boundary applies (2 + 2), y copy (K5 kernels) — NCCL's own excluded
+            "gpu_launches": args.steps * (2 if world == 1 else 6),
             "clocks": clk.summary(),
             "cpu_baseline": cb,
             "fused": fused_flag,

@@ -22,6 +22,25 @@ import torch
 import torch.distributed as dist
 
 
+def layers_copy(dst, src, add=False):
+    """dst (+)= src over contiguous DoF layers: the K5 halo kernel
+    (igs_layers_copy) on the device, torch on the CPU (gloo tests)."""
+    n = src.numel()
+    if n == 0:
+        return dst
+    if dst.is_cuda:
+        from . import _lib
+
+        lib = _lib.load()
+        _lib.check(lib.igs_layers_copy(_lib.ptr(src), _lib.ptr(dst), n, int(bool(add)), _lib.stream_handle()),
+                   "layers_copy")
+    elif add:
+        dst.add_(src)
+    else:
+        dst.copy_(src)
+    return dst
+
+
 class SlabPartition:
     """Balanced split of K elements (last direction) over `world` ranks."""
 
@@ -101,7 +120,7 @@ class ShardedApply:
     def apply(self, x_own, y_own=None):
         """y_own = (A x) restricted to this rank's own DoF layers."""
         r, W, g = self.rank, self.part.world, (self.part.p - 1) * self.layer
-        self.x_local[: self.n_own].copy_(x_own)
+        layers_copy(self.x_local[: self.n_own], x_own)
         # 1. ghost gather: my first p-1 own layers go to r-1; r+1's come to me.
         send, recv = [], []
         if r > 0 and g:
@@ -134,10 +153,9 @@ class ShardedApply:
         self._exchange(send, recv)
         out = self.y_local[: self.n_own]
         if r > 0 and g:
-            out[:g] += self.halo_in
+            layers_copy(out[:g], self.halo_in, add=True)
         if y_own is not None:
-            y_own.copy_(out)
-            return y_own
+            return layers_copy(y_own, out)
         return out
 
 

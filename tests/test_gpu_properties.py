@@ -325,3 +325,30 @@ def test_host_pipeline_matches_sequential_applies(cuda):
     for xh, yh in zip(xs, ys):
         ref = op.apply_device(xh.cuda()).cpu()
         assert torch.equal(yh, ref)
+
+
+def test_layers_copy_kernel_and_single_rank_sharded_apply(cuda):
+    """K5 halo kernel (igs_layers_copy) behind sharded.layers_copy, and a
+    world-1 ShardedApply (no exchange) equal to the plain apply."""
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    from paper_1809_05471_b200.sharded import ShardedApply, SlabPartition, layers_copy
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(1000, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(1000, dtype=torch.float64, device="cuda", generator=g)
+    ref = a + b
+    layers_copy(b, a, add=True)
+    assert torch.equal(b, ref)
+    layers_copy(b[:10], a[:10])
+    assert torch.equal(b[:10], a[:10]) and torch.equal(b[10:], ref[10:])
+    d, p, K = 3, 4, 5
+    prob = workloads.make_problem(d, p, K, 3, seed=2)
+    op = matfree.MatrixFreeOperator(prob)
+    N = prob.shape[1]
+    layer = N // (K + p - 1)
+    x = torch.randn(N, dtype=torch.float64, device="cuda", generator=g)
+    sh = ShardedApply(SlabPartition(K, p, 1), 0, layer, lambda xl, yl: op.apply_device(xl, yl), "cuda")
+    y = torch.empty_like(x)
+    sh.apply(x, y)
+    assert torch.equal(y, op.apply_device(x, torch.empty_like(x)))
