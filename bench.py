@@ -195,18 +195,22 @@ def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
     #   asm3_stage12, per (4x4-row tile, z point): stage 1 = 4 y-tiles x 4
     #   slot tiles x 10 blocks x 4 k-steps = 640 DMMA, stage 2 = 4 x 4 x 9
     #   groups x 4 = 576 DMMA (512 flop each), over 17^2 tiles;
-    #   asm_sweep: 4 FMA per (slot pair, z point, jm, jn), slot pairs padded
-    #   to blocks of 128.
+    #   asm_sweep, per (slot pair, z point): the separable last-direction
+    #   contraction, 2P (mul + FMA) for u_0/u_1 and 2P^2 FMA into the ring
+    #   = 6P + 4P^2 flops; slot pairs padded to blocks of 128.
     e_cnt = e_hi - e_lo
     n_tiles = (-(-67 // 4)) ** 2
     stage12 = 512 * (640 + 576) * n_tiles * (e_cnt * p)
     slot_pairs = -(-(67 * 7) ** 2 // 128) * 128
-    sweep = 2 * 4 * p * p * slot_pairs * (e_cnt * p)
+    sweep = (6 * p + 4 * p * p) * slot_pairs * (e_cnt * p)
     f_exec = float(stage12 + sweep)
     if world > 1:
         tt = torch.tensor([f_exec], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt)
         f_exec = float(tt.item())
+    # per-kernel composition: stage12 at the DMMA peak + the sweep's compulsory
+    # traffic (H read once, values written once) at the copy bandwidth
+    sweep_bytes = 8 * slot_pairs * (e_cnt * p) * 4 + 8 * nnz
     f_merged = 2 * 10_390_000_000        # merged-block MACs (the algorithm's own count)
     f_ref = 2 * 16_030_801_920           # the reference FlopCounter's block updates
     p64 = 37.15e12 * world               # measured DMMA peak per GPU (profiles/r01_fp64_peak.txt)
@@ -219,7 +223,32 @@ def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
                         "frac": max(f_exec / t / p64, b_alg / t / (peak_bw * 1e9 * world)),
                         "exec_flops": f_exec, "alg_flops_merged": f_merged, "ref_flops": f_ref,
                         "frac_merged_alg": f_merged / t / p64, "frac_ref_equivalent": f_ref / t / p64,
-                        "hbm_gbs": b_alg / t / 1e9, "alg_bytes": b_alg}}
+                        "hbm_gbs": b_alg / t / 1e9, "alg_bytes": b_alg,
+                        "frac_kernel_composed": (stage12 / (37.15e12) + sweep_bytes / (peak_bw * 1e9)) / world / t}}
+    # cold assembly (fresh problem: tabulation + pattern + values) and the CSR
+    # hand-off to the host (f2), reported separately as SURVEY §8(d) asks
+    if world == 1:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cold = AssemblyProblem(bases, bases, quad, field, max_nnz=1 << 40)
+        A = sumfac.assemble(cold)
+        torch.cuda.synchronize()
+        out["cold_ms"] = (time.perf_counter() - t0) * 1e3
+        pat = cold.pattern()
+        hv = torch.empty(A.values.shape, dtype=A.values.dtype, pin_memory=True)
+        hi_ = torch.empty(pat.indices_dev.shape, dtype=pat.indices_dev.dtype, pin_memory=True)
+        hp = torch.empty(pat.indptr_dev.shape, dtype=pat.indptr_dev.dtype, pin_memory=True)
+        e0.record()
+        hv.copy_(A.values, non_blocking=True)
+        hi_.copy_(pat.indices_dev, non_blocking=True)
+        hp.copy_(pat.indptr_dev, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        d2h_ms = e0.elapsed_time(e1)
+        nbytes = hv.numel() * 8 + hi_.numel() * hi_.element_size() + hp.numel() * 8
+        out["csr_d2h"] = {"ms": d2h_ms, "bytes": nbytes, "gbs": nbytes / d2h_ms / 1e6,
+                          "index_bytes": hi_.element_size()}
+        del A, cold, hv, hi_, hp
     if cpu and rank == 0 and world == 1:
         from oracle import igs_oracle as O
 
