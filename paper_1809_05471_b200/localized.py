@@ -256,7 +256,7 @@ def _local_positions(pattern_g, ls, lpat):
     with r_δ the offset of n_δ in the 1D row m_δ and w_δ its width."""
     torch = _lib.require_cuda()
     rows = torch.repeat_interleave(torch.arange(lpat.shape[0], device="cuda"), torch.diff(lpat.indptr_dev))
-    mrem, nrem = rows, lpat.indices_dev
+    mrem, nrem = rows, lpat.indices_dev.long()
     m_flat = torch.zeros_like(rows)
     stride = 1
     per_dir = []

@@ -139,8 +139,9 @@ class DirectionPairs:
 class SparsityPattern:
     """Tensor-product CSR pattern shared by all derivative blocks (tensorspace.py:262-338).
 
-    `indptr_dev` / `indices_dev` are device int64 tensors; `indptr` /
-    `indices` are host copies made on first access.
+    `indptr_dev` (int64) / `indices_dev` (int32 when the columns fit, else
+    int64) are device tensors; `indptr` / `indices` (int64) are host copies
+    made on first access.
     """
 
     def __init__(self, dir_pairs, trial_dims, test_dims, indptr_dev, indices_dev, nnz):
@@ -189,7 +190,13 @@ class SparsityPattern:
     def to_torch(self, values):
         torch = _lib.require_cuda()
         m, n = self.shape
-        return torch.sparse_csr_tensor(self.indptr_dev, self.indices_dev, values, size=(m, n))
+        ip, ix = self.indptr_dev, self.indices_dev
+        if ip.dtype != ix.dtype:  # cuSPARSE wants one index type
+            key = "torch_idx"
+            if key not in self._host:
+                self._host[key] = (ip.to(torch.int32), ix) if self.nnz < 2 ** 31 else (ip, ix.to(torch.int64))
+            ip, ix = self._host[key]
+        return torch.sparse_csr_tensor(ip, ix, values, size=(m, n))
 
 
 def _direction_bases(system):
@@ -266,13 +273,19 @@ def tensor_pattern(trial, test, quad, max_nnz=DEFAULT_MAX_PATTERN_NNZ):
     for b in test_bases:
         nrows *= b.num_basis
     indptr = torch.empty(nrows + 1, dtype=torch.int64, device="cuda")
-    indices = torch.empty(total, dtype=torch.int64, device="cuda")
+    ncols = 1
+    for b in trial_bases:
+        ncols *= b.num_basis
+    # int32 columns whenever they fit (2/3 of the index bytes; the host copy
+    # is widened to the reference's int64)
+    ib = 4 if ncols < 2 ** 31 else 8
+    indices = torch.empty(total, dtype=torch.int32 if ib == 4 else torch.int64, device="cuda")
     rp = (ctypes.c_void_p * 3)(*[dp.rowptr_dev.data_ptr() for dp in pairs] + [0] * (3 - len(pairs)))
     cl = (ctypes.c_void_p * 3)(*[dp.cols_dev.data_ptr() for dp in pairs] + [0] * (3 - len(pairs)))
     for k, dp in enumerate(pairs):
         prob.num_pairs[k] = dp.num_pairs
     st = lib.igs_pattern(ctypes.byref(prob), rp, cl, 0, nrows, 0, _lib.ptr(indptr),
-                         _lib.ptr(indices) if total else None, 8, _lib.stream_handle())
+                         _lib.ptr(indices) if total else None, ib, _lib.stream_handle())
     _lib.check(st, "pattern")
     return SparsityPattern(pairs, [b.num_basis for b in trial_bases], [b.num_basis for b in test_bases],
                            indptr, indices, total)
