@@ -240,6 +240,29 @@ igs_status igs_geometry_pullback(const igs_pullback_args* args, const int8_t* pl
                                  uint32_t* nonzero, int64_t* bad /* host */, void* ws, size_t ws_bytes,
                                  void* stream);
 
+/* f1 fused: the map's spline fields evaluated in place at every point (sum
+ * over its active control points of the tensor basis from its 1D value /
+ * first-derivative tables at the quadrature points; rational maps by the
+ * quotient rule) and pulled back in the same pass — only the planes (and
+ * optionally phys) are written, no field arrays.  PDE data, npts and rtol
+ * come from `pde` (its val/grad/wval/wgrad are ignored); outputs and the
+ * degeneracy verdict as igs_geometry_pullback.  Map orders 2..8. */
+typedef struct {
+  int32_t d;
+  int32_t order[IGS_MAX_DIM];          /* map basis orders                           */
+  int32_t num_basis[IGS_MAX_DIM];      /* map basis counts (control grid, dir 0 fastest) */
+  int64_t num_points[IGS_MAX_DIM];     /* quadrature points per direction            */
+  const double* values[IGS_MAX_DIM];   /* [2][order][num_points]: B and dB/dx tables  */
+  const int64_t* first_active[IGS_MAX_DIM];
+  const double* control;               /* [num control points][d]                    */
+  const double* weights;               /* [num control points] or NULL (polynomial)  */
+} igs_geometry_map;
+
+igs_status igs_geometry_planes(const igs_geometry_map* map, const igs_pullback_args* pde,
+                               const int8_t* plane_of /* host */, int32_t n_planes, double* planes,
+                               int64_t plane_stride, double* phys, uint32_t* nonzero, int64_t* bad /* host */,
+                               void* ws, size_t ws_bytes, void* stream);
+
 /* ---- K5: halo pack / unpack-add for the slab-partitioned apply ------- */
 /* Copies `nlayers` contiguous DoF layers (layer = N0*N1 doubles) — kept
  * as kernels so they can be captured in CUDA graphs. dst[i] (+)= src[i]. */

@@ -83,6 +83,19 @@ class IgsPullbackArgs(ctypes.Structure):
     ]
 
 
+class IgsGeometryMap(ctypes.Structure):
+    _fields_ = [
+        ("d", ctypes.c_int32),
+        ("order", ctypes.c_int32 * MAX_DIM),
+        ("num_basis", ctypes.c_int32 * MAX_DIM),
+        ("num_points", ctypes.c_int64 * MAX_DIM),
+        ("values", ctypes.c_void_p * MAX_DIM),
+        ("first_active", ctypes.c_void_p * MAX_DIM),
+        ("control", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) for every symbol declared in include/igs_capi.h.
 _SIGNATURES = [
     ("igs_last_error", ctypes.c_char_p, []),
@@ -122,6 +135,10 @@ _SIGNATURES = [
      [ctypes.POINTER(IgsProblem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
       ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
       ctypes.c_void_p]),
+    ("igs_geometry_planes", ctypes.c_int,
+     [ctypes.POINTER(IgsGeometryMap), ctypes.POINTER(IgsPullbackArgs), ctypes.c_void_p, ctypes.c_int32,
+      ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+      ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     ("igs_geometry_pullback", ctypes.c_int,
      [ctypes.POINTER(IgsPullbackArgs), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_size_t,

@@ -421,15 +421,11 @@ def _coeff_device(spec, shape, d, geo_eval):
     return torch.broadcast_to(t, shape).contiguous(), False
 
 
-def build_coefficient_field(geo_eval, pde, counter=None):
-    """Pull a second-order form back through an evaluated geometry
-    (geometry.py:315-336) into device coefficient planes: F = |det J|·E·
-    [[c, 0], [b, A]]·E^T, E = diag(1, J^{-1}); exactly-zero blocks are
-    dropped (geometry.py:296), transposed blocks of a symmetric diffusion
-    share a plane."""
+def _plane_setup(pde, d, geo_eval):
+    """Device PDE data, the plane map over (eta i, theta j) of the first-order
+    set and the kernel pointer tuple.  `geo_eval` provides num_points and, for
+    callables, phys."""
     torch = _lib.require_cuda()
-    d = geo_eval.d
-    npts = geo_eval.num_points
     A, a_pp = _coeff_device(pde.diffusion, (d, d), d, geo_eval)
     b, b_pp = _coeff_device(pde.convection, (d,), d, geo_eval)
     c, c_pp = _coeff_device(pde.reaction, (), d, geo_eval)
@@ -451,7 +447,6 @@ def build_coefficient_field(geo_eval, pde, counter=None):
             for j in range(d):
                 diff[i][j] = At[i, j].data_ptr()
         sym = all(torch.equal(At[i, j], At[j, i]) for i in range(d) for j in range(i + 1, d))
-    # plane map over (eta i, theta j) of the first-order set
     n = d + 1
     plane_of = [[-1] * n for _ in range(n)]
     npl = 0
@@ -470,14 +465,16 @@ def build_coefficient_field(geo_eval, pde, counter=None):
                 else:
                     plane_of[1 + i][1 + j] = npl
                     npl += 1
-    planes = torch.empty((max(npl, 1), npts), dtype=torch.float64, device="cuda")
     ptrs = (cptr, 1 if c_pp else 0, conv, 1 if b_pp else 0, diff, 1 if a_pp else 0)
-    bad, nonzero = _pullback(geo_eval._f, npts, plane_of, npl, ptrs, planes=planes, keep=keep)
-    if bad >= 0:
-        _raise_degenerate(geo_eval.quad, bad)
+    return plane_of, npl, ptrs, keep
+
+
+def _plane_finish(planes, plane_of, npl, nonzero, d, npts, point_shape, counter):
+    """Drop exactly-zero planes (geometry.py:296), renumber, wrap."""
+    torch = _lib.require_cuda()
     if counter is not None:
         counter.add_coeff_build(npts * (2 * (1 + d) ** 3 + (1 + d) ** 2))
-    # drop exactly-zero planes, renumber
+    n = d + 1
     live = [p for p in range(npl) if nonzero[p]]
     remap = {p: k for k, p in enumerate(live)}
     plane_of = [[remap.get(plane_of[i][j], -1) if plane_of[i][j] >= 0 else -1 for j in range(n)] for i in range(n)]
@@ -486,7 +483,121 @@ def build_coefficient_field(geo_eval, pde, counter=None):
     elif not live:
         planes = torch.zeros((0, npts), dtype=torch.float64, device="cuda")
     ths = first_order_derivative_set(d)
-    return CoefficientField.from_planes(ths, ths, planes, plane_of, geo_eval.point_shape)
+    return CoefficientField.from_planes(ths, ths, planes, plane_of, point_shape)
+
+
+def build_coefficient_field(geo_eval, pde, counter=None):
+    """Pull a second-order form back through an evaluated geometry
+    (geometry.py:315-336) into device coefficient planes: F = |det J|·E·
+    [[c, 0], [b, A]]·E^T, E = diag(1, J^{-1}); exactly-zero blocks are
+    dropped (geometry.py:296), transposed blocks of a symmetric diffusion
+    share a plane."""
+    torch = _lib.require_cuda()
+    d = geo_eval.d
+    npts = geo_eval.num_points
+    plane_of, npl, ptrs, keep = _plane_setup(pde, d, geo_eval)
+    planes = torch.empty((max(npl, 1), npts), dtype=torch.float64, device="cuda")
+    bad, nonzero = _pullback(geo_eval._f, npts, plane_of, npl, ptrs, planes=planes, keep=keep)
+    if bad >= 0:
+        _raise_degenerate(geo_eval.quad, bad)
+    return _plane_finish(planes, plane_of, npl, nonzero, d, npts, geo_eval.point_shape, counter)
+
+
+class _MapPoints:
+    """The fused path's view of the map at the quadrature points: tables,
+    control data and the C struct; `phys` (for callable PDE data) by one
+    plane-less pass of the fused kernel."""
+
+    def __init__(self, geo, quad):
+        torch = _lib.require_cuda()
+        self.geo, self.quad = geo, quad
+        self.d = geo.d
+        self.point_shape = tuple(quad.shape)
+        self.num_points = quad.num_points
+        for basis in geo.bases:
+            if not 2 <= basis.order <= 8:
+                raise ValueError("fused geometry evaluation needs map orders 2..8")
+        self.tables = [tabulate(b, r.points, 1) for b, r in zip(geo.bases, quad.rules)]
+        self.control = torch.as_tensor(np.ascontiguousarray(geo.control_points), dtype=torch.float64,
+                                       device="cuda").contiguous()
+        self.weights = (torch.as_tensor(np.asarray(geo.weights, dtype=float), device="cuda")
+                        if geo.is_rational else None)
+        m = _lib.IgsGeometryMap()
+        m.d = self.d
+        for k, (b, t) in enumerate(zip(geo.bases, self.tables)):
+            m.order[k] = b.order
+            m.num_basis[k] = b.num_basis
+            m.num_points[k] = quad.rules[k].num_points
+            m.values[k] = t.values.data_ptr()
+            m.first_active[k] = t.first_active.data_ptr()
+        m.control = self.control.data_ptr()
+        m.weights = self.weights.data_ptr() if self.weights is not None else None
+        self.struct = m
+        self._phys = None
+
+    def run(self, plane_of, npl, ptrs, planes=None, phys=None, keep=()):
+        import ctypes
+
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        d = self.d
+        args = _lib.IgsPullbackArgs()
+        args.d = d
+        args.npts = self.num_points
+        (args.reaction, args.reaction_stride, conv, args.convection_stride, diff,
+         args.diffusion_stride) = ptrs
+        for i in range(d):
+            args.convection[i] = conv[i]
+            for j in range(d):
+                args.diffusion[i][j] = diff[i][j]
+        args.rtol = _DEGENERACY_RTOL
+        pm = (ctypes.c_int8 * 16)(*[plane_of[i][j] if (i < len(plane_of) and j < len(plane_of)) else -1
+                                    for i in range(4) for j in range(4)])
+        flags = torch.zeros(max(npl, 1), dtype=torch.int32, device="cuda")
+        ws = torch.empty(64, dtype=torch.uint8, device="cuda")
+        bad = ctypes.c_int64(-1)
+        st = lib.igs_geometry_planes(ctypes.byref(self.struct), ctypes.byref(args), pm, npl,
+                                     planes.data_ptr() if planes is not None else None,
+                                     int(planes.stride(0)) if planes is not None else 0,
+                                     phys.data_ptr() if phys is not None else None, flags.data_ptr(),
+                                     ctypes.byref(bad), ws.data_ptr(), 64, _lib.stream_handle())
+        _lib.check(st, "geometry_planes")
+        del keep
+        if bad.value >= 0:
+            _raise_degenerate(self.quad, int(bad.value))
+        return flags[:npl].cpu().numpy()
+
+    @property
+    def phys(self):
+        if self._phys is None:
+            torch = _lib.require_cuda()
+            ph = torch.empty((self.d, self.num_points), dtype=torch.float64, device="cuda")
+            nop = (None, 0, [None] * 3, 0, [[None] * 3 for _ in range(3)], 0)
+            self.run([], 0, nop, phys=ph)
+            self._phys = ph.t().cpu().numpy()
+        return self._phys
+
+
+def pull_back_fused(geo, quad, pde, counter=None):
+    """f1 fused: coefficient planes straight from the map and the PDE data
+    (one kernel pass evaluates the map's fields per point and pulls back;
+    no per-point field arrays) — the same planes as
+    build_coefficient_field(eval_geometry(geo, quad), pde) up to rounding."""
+    torch = _lib.require_cuda()
+    mp = _MapPoints(geo, quad)
+    d, npts = mp.d, mp.num_points
+    plane_of, npl, ptrs, keep = _plane_setup(pde, d, mp)
+    planes = torch.empty((max(npl, 1), npts), dtype=torch.float64, device="cuda")
+    nonzero = mp.run(plane_of, npl, ptrs, planes=planes, keep=keep)
+    if counter is not None:
+        # the reference's count for the fields the two-step path evaluates
+        # (value + d derivatives per component, and the weight if rational)
+        from .tensorspace import field_eval_count
+
+        per = field_eval_count([b.order for b in geo.bases], [b.num_basis for b in geo.bases],
+                               [r.num_points for r in quad.rules])
+        counter.add_field_eval(per * (d + 1) * (geo.s + (1 if geo.is_rational else 0)))
+    return _plane_finish(planes, plane_of, npl, nonzero, d, npts, mp.point_shape, counter)
 
 
 class PulledBackCoefficient:
@@ -499,7 +610,11 @@ class PulledBackCoefficient:
         self.theta_set = first_order_derivative_set(geometry.d)
         self.eta_set = self.theta_set
 
-    def evaluate(self, quad, counter=None):
+    def evaluate(self, quad, counter=None, fused=True):
+        """fused=True: pull_back_fused (map orders 2..8); else the two-step
+        eval_geometry (Alg. 3 field arrays) + build_coefficient_field."""
+        if fused and all(2 <= b.order <= 8 for b in self.geometry.bases):
+            return pull_back_fused(self.geometry, quad, self.pde, counter)
         return build_coefficient_field(eval_geometry(self.geometry, quad, counter), self.pde, counter)
 
 
