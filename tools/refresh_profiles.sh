@@ -15,4 +15,7 @@ ncu --set full --import-source on --clock-control none -k regex:apply3d_kernel -
     -o $O/prof_c5 python tools/time_apply.py C5 > $O/ncu_c5.log 2>&1
 ncu --set full --import-source on --clock-control none -k "regex:asm3_stage12|asm_sweep" -s 2 -c 2 \
     -o $O/prof_asm_c3 python tools/prof_asm.py C3 > $O/ncu_asm.log 2>&1
+python tools/f1_time.py 128 > $O/f1_c4_grid.txt 2>&1
+ncu --set full --import-source on --clock-control none -k regex:geom_line_kernel -s 1 -c 1 \
+    -o $O/prof_f1 python tools/f1_time.py 64 > $O/ncu_f1.log 2>&1
 ls -la $O
