@@ -102,3 +102,67 @@ def test_sharded_apply_matches_single_process(world, d, p, K, kind, split):
     assert y.size == n
     assert np.linalg.norm(y - y_ref) / np.linalg.norm(y_ref) <= 1e-14
     del layer_n
+
+
+def _cg_worker(rank, world, port, d, p, K, kind, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1809_05471_b200.sharded import ShardedApply, SlabPartition
+    from paper_1809_05471_b200.solvers import cg
+
+    sp = [O.uniform_space(p, K) for _ in range(d)]
+    shape = [p * K] * d
+    ths = O.first_order_set(d)
+    pm = O.plane_map(d, kind)
+    n = int(np.prod([s.num_basis for s in sp]))
+    layer_n = n // (K + p - 1)
+    part = SlabPartition(K, p, world)
+    lo, hi = part.elements(rank)
+    planes = O.synthetic_planes(d, shape, lo * p, hi * p, kind, seed=9)
+
+    def compute(xl, yl):
+        full = np.zeros(n)
+        full[lo * layer_n: lo * layer_n + xl.numel()] = xl.numpy()
+        yl.copy_(torch.from_numpy(O.apply_slab(sp, p, ths, ths, pm, planes, full, lo, hi)))
+
+    sa = ShardedApply(part, rank, layer_n, compute, "cpu")
+    olo, ohi = part.own_layers(rank)
+    b = torch.from_numpy(O.recipe_x(n, seed=5)[olo * layer_n: ohi * layer_n].copy())
+    x, it, res = cg(lambda v, out: out.copy_(sa.apply(v)), b, tol=1e-12, maxiter=1000, group=dist.group.WORLD)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (olo, x.numpy(), it, res))
+    if rank == 0:
+        q.put(gathered)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,d,p,K,kind", [(2, 2, 3, 8, 3), (3, 2, 4, 9, 3)])
+def test_sharded_cg_matches_direct_solve(world, d, p, K, kind):
+    """CG on the slab-partitioned apply, the inner products
+    all-reduced over the group — the gathered solution equals the direct solve."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cg_worker, args=(r, world, port, d, p, K, kind, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    gathered = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    its = {g[2] for g in gathered}
+    assert len(its) == 1  # every rank saw the same global residuals
+    assert all(g[3] <= 1e-12 for g in gathered)
+    sp = [O.uniform_space(p, K) for _ in range(d)]
+    shape = [p * K] * d
+    n = int(np.prod([s.num_basis for s in sp]))
+    planes = O.synthetic_planes(d, shape, 0, shape[-1], kind, seed=9)
+    ths = O.first_order_set(d)
+    pm = O.plane_map(d, kind)
+    A = np.stack([O.apply(sp, p, ths, ths, pm, planes, e) for e in np.eye(n)], axis=1)
+    b = O.recipe_x(n, seed=5)
+    x_ref = np.linalg.solve(A, b)
+    x = np.concatenate([g[1] for g in sorted(gathered, key=lambda t: t[0])])
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-9
