@@ -759,7 +759,15 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
 // Row tile per direction of the 3D stage-1/2 kernel: the largest of 4, 2, 1
 // whose shared-memory plan fits (0 = none).
 template <int P>
+constexpr int kWideTile = P == 2 ? 10 : P == 3 ? 6 : 0;
+
+template <int P>
 int asm3_tile(const AsmPlan& pl, int nplanes) {
+  // low orders: wider tiles so both stages have >= 16 warp tasks (and, for
+  // p = 3, a region of whole MMA row tiles); else the largest of 4, 2, 1
+  constexpr int wide = kWideTile<P>;
+  if constexpr (wide > 0)
+    if (A3Cfg<P, P, wide>::smem(nplanes, pl.ng) <= 232448) return wide;
   if (A3Cfg<P, P, 4>::smem(nplanes, pl.ng) <= 232448) return 4;
   if (A3Cfg<P, P, 2>::smem(nplanes, pl.ng) <= 232448) return 2;
   if (A3Cfg<P, P, 1>::smem(nplanes, pl.ng) <= 232448) return 1;
@@ -938,12 +946,14 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   if (row_hi <= row_lo) return IGS_OK;
   ZRange z;
   IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
-  switch (asm3_tile<P>(s.plan, p->n_planes)) {
-    case 4: IGS_TRY((launch3_stage12<P, Q, 4>(p, s, z, planes, H, st))); break;
-    case 2: IGS_TRY((launch3_stage12<P, Q, 2>(p, s, z, planes, H, st))); break;
-    case 1: IGS_TRY((launch3_stage12<P, Q, 1>(p, s, z, planes, H, st))); break;
-    default: return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
+  const int tile = asm3_tile<P>(s.plan, p->n_planes);
+  if (tile == 0) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
+  if constexpr (kWideTile<P> > 0) {
+    if (tile == kWideTile<P>) IGS_TRY((launch3_stage12<P, Q, kWideTile<P>>(p, s, z, planes, H, st)));
   }
+  if (tile == 4) IGS_TRY((launch3_stage12<P, Q, 4>(p, s, z, planes, H, st)));
+  else if (tile == 2) IGS_TRY((launch3_stage12<P, Q, 2>(p, s, z, planes, H, st)));
+  else if (tile == 1) IGS_TRY((launch3_stage12<P, Q, 1>(p, s, z, planes, H, st)));
   constexpr int W = 2 * P - 1;
   struct {
     int64_t NS0, NS1;

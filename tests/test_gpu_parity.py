@@ -263,9 +263,11 @@ def test_apply_tiny_and_ragged_meshes_vs_oracle(cuda, p, K, kind):
 
 @pytest.mark.parametrize("d,p,K,kind", [(3, 2, (1, 1, 1), 3), (3, 4, (1, 2, 3), 3), (3, 3, (2, 5, 1), 2),
                                         (3, 5, (2, 1, 2), 3), (3, 6, (1, 1, 2), 2), (2, 5, (1, 3), 3),
-                                        (2, 4, (9, 1), 1)])
+                                        (2, 4, (9, 1), 1), (3, 3, (14, 9, 3), 3), (3, 2, (13, 21, 2), 3),
+                                        (3, 4, (9, 6, 3), 3)])
 def test_assembly_tiny_and_ragged_meshes_vs_oracle(cuda, d, p, K, kind):
-    """Assembly on meshes smaller than one row tile, fused and generic, against
+    """Assembly on meshes smaller than one row tile and on ragged multi-tile
+    meshes (the wide p = 2, 3 tiles included), fused and generic, against
     the oracle's independent Kronecker assembly (pattern identical)."""
     *_, sumfac, matfree, workloads = _pkg()
     from paper_1809_05471_b200.bspline import UnivariateBasis, uniform_open_knots
