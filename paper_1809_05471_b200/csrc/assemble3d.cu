@@ -660,14 +660,25 @@ struct Asm2Args {
   int64_t NE;      // elements of the last direction (K1)
   int nt0;         // row tiles in x
   int yc;          // y points per CTA (multiple of A2_YS)
+  const double* Wg;  // [nt0][W0T] band tables, built once per assembly (asm2_tables_kernel)
 };
+
+// The 2D tiles' band tables, one block per row tile, built once per
+// assembly: the stage-1 CTAs (several per tile, one per y chunk) then
+// bulk-copy theirs instead of recomputing it.
+template <int P, int Q, int T>
+__global__ void asm2_tables_kernel(const TabArgs tab, double* Wg) {
+  using C = A3Cfg<P, Q, T>;
+  const int a0 = blockIdx.x * T;
+  fill_band_table<P, Q, T, false>(Wg + (size_t)blockIdx.x * C::W0T, tab, 0, a0, (a0 - (P - 1)) * Q);
+}
 
 // 2D stage 1 as a dense banded GEMM on DMMA (the 3D stage-1 structure):
 // one CTA per (T-row tile in x, chunk of y points); the tile's band table
 // W0[v][x][slot] is built once and reused for every y block; coefficient
 // boxes of A2_YS y rows x the tile's x region (all planes) stream in by
 // TMA, double-buffered.  G_g[y][s0] = Σ_{b∈g} Σ_x F_b[y][x] W0^{v0(b)}[x][s0].
-constexpr int A2_YS = 64, A2_NT = 256, A2_NW = 8;
+constexpr int A2_YS = 64, A2_NT = 512, A2_NW = 16;
 template <int P, int Q, int T>
 struct A2Cfg {
   using B = A3Cfg<P, Q, T>;
@@ -700,17 +711,27 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
   const unsigned fbytes = (unsigned)((size_t)nplanes * A2_YS * XR * sizeof(double));
   for (int b = 0; b < 2; ++b)
     for (size_t i = (size_t)nplanes * A2_YS * XR + tid; i < fb; i += A2_NT) Fs[b * fb + i] = 0.0;
-  if (tid < 2) dev::mbar_init(bar + tid, 1);
+  if (tid < 3) dev::mbar_init(bar + tid, 1);
   dev::fence_mbar_init();
   dev::fence_proxy_async();
   __syncthreads();
-  if (tid == 0)
+  if (tid == 0) {
+    if (a.Wg) {
+      constexpr unsigned wbytes = (unsigned)(C::W0T * sizeof(double));
+      dev::mbar_expect_tx(bar + 2, wbytes);
+      dev::bulk_load(W0, a.Wg + (size_t)(blockIdx.x % a.nt0) * C::W0T, wbytes, bar + 2);
+    }
     for (int i = 0; i < 2 && i < nstage; ++i) {
       dev::mbar_expect_tx(bar + i, fbytes);
       dev::tma_load_4d(Fs + i * fb, &fmap, bar + i, xb0, (int)(y_lo + i * A2_YS), 0, 0);
     }
-  fill_band_table<P, Q, T, false>(W0, a.tab, 0, a0, xb0);
-  __syncthreads();
+  }
+  if (a.Wg) {
+    dev::mbar_wait(bar + 2, 0u);
+  } else {
+    fill_band_table<P, Q, T, false>(W0, a.tab, 0, a0, xb0);
+    __syncthreads();
+  }
   for (int i = 0; i < nstage; ++i) {
     const int buf = i & 1;
     dev::mbar_wait(bar + buf, (unsigned)((i >> 1) & 1));
@@ -795,6 +816,30 @@ int asm2_tile(int nplanes) {
   return 0;
 }
 
+// Upper bound over the row tiles T of the band-table store (bytes).
+template <int P>
+size_t asm2_tables_bytes(int64_t nfn0) {
+  const size_t t8 = (size_t)ceil_div(nfn0, 8) * A3Cfg<P, P, 8>::W0T;
+  const size_t t4 = (size_t)ceil_div(nfn0, 4) * A3Cfg<P, P, 4>::W0T;
+  const size_t t2 = (size_t)ceil_div(nfn0, 2) * A3Cfg<P, P, 2>::W0T;
+  const size_t t1 = (size_t)nfn0 * A3Cfg<P, P, 1>::W0T;
+  size_t m = t8 > t4 ? t8 : t4;
+  m = m > t2 ? m : t2;
+  m = m > t1 ? m : t1;
+  return m * sizeof(double);
+}
+
+size_t asm2_tables_bytes_for(int P, int64_t nfn0) {
+  switch (P) {
+    case 2: return asm2_tables_bytes<2>(nfn0);
+    case 3: return asm2_tables_bytes<3>(nfn0);
+    case 4: return asm2_tables_bytes<4>(nfn0);
+    case 5: return asm2_tables_bytes<5>(nfn0);
+    case 6: return asm2_tables_bytes<6>(nfn0);
+    default: return 0;
+  }
+}
+
 int asm2_tile_for(int P, int nplanes) {
   switch (P) {
     case 2: return asm2_tile<2>(nplanes);
@@ -872,7 +917,8 @@ size_t asm_workspace(const AsmShape& s) {
            (size_t)s.fs.nel[2] * (s.fs.k * 4 * (s.fs.p + 1) + 4) * sizeof(double) + 512;
   }
   return padded(s.fs.nfn[0] * W) * s.fs.npt[1] * s.plan.ng * sizeof(double) +
-         (size_t)s.fs.nel[1] * (s.fs.k * 4 * (s.fs.p + 1) + 4) * sizeof(double) + 512;
+         ((size_t)s.fs.nel[1] * (s.fs.k * 4 * (s.fs.p + 1) + 4) + 2) * sizeof(double) +
+         asm2_tables_bytes_for(s.fs.p, s.fs.nfn[0]) + 512;
 }
 
 // z elements the row range needs (rows of DoF layers [m2a, m2b] are summed
@@ -1020,6 +1066,17 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
   yc = ceil_div(yc, A2_YS) * A2_YS;
   a.yc = (int)yc;
   const int64_t nyc = ceil_div(s.fs.npt[1], yc);
+  // band tables after the G region and the last-direction element records
+  const int64_t nbsp = ceil_div(a.NS0, (int64_t)kSweepBlock);
+  double* Wg = G + (size_t)nbsp * kSweepBlock * s.fs.npt[1] * s.plan.ng +
+               (((size_t)s.fs.nel[1] * S3Cfg<P, Q>::NWR + 1) & ~size_t(1));
+  // GPU-filling grids share one table per tile (built once); small grids
+  // (launch-bound, e.g. C1) fill it in the CTA and skip the extra launch
+  if (a.nt0 * nyc >= 2 * 148) {
+    asm2_tables_kernel<P, Q, T><<<(unsigned)a.nt0, 256, 0, st>>>(a.tab, Wg);
+    IGS_LAUNCH_CHECK("asm2_tables_kernel");
+    a.Wg = Wg;
+  }
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm2_stage1<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem),
                      "smem attribute"));

@@ -1,4 +1,4 @@
-"""Parity at BASELINE.json's full sizes (C3 assembly, C4 / C5 applies).
+"""Parity at BASELINE.json's full sizes (C2 / C3 assembly, C4 / C5 applies).
 
 The oracle cannot run these sizes whole, so the checks are the
 size-independent properties the domain offers, plus a full-width spot check
@@ -94,3 +94,20 @@ def test_full_size_c3_assembly_fused_vs_generic_and_measure(cuda):
     Au, Av = A.matvec(u), A.matvec(v)
     nrm = float(torch.linalg.vector_norm(u) * torch.linalg.vector_norm(Av))
     assert abs(float(torch.dot(v, Au) - torch.dot(u, Av))) <= 1e-12 * nrm
+
+
+def test_full_size_c2_assembly_fused_vs_generic(cuda):
+    """C2 (d=2, p=5, 256², stiffness): the fused 2D path at a GPU-filling
+    grid (shared precomputed band tables) against the stage kernels."""
+    torch = cuda
+    matfree, sumfac, workloads = _mods()
+    prob = workloads.make_problem(2, 5, 256, workloads.STIFF, seed=0)
+    A = sumfac.assemble(prob)
+    assert sumfac.fused_path(prob) == 1
+    assert A.nnz == 5_382_400
+    B = sumfac.assemble(prob, flags=1)
+    err = float(torch.linalg.vector_norm(A.values - B.values) / torch.linalg.vector_norm(B.values))
+    assert err <= 1e-12
+    n = prob.shape[1]
+    one = torch.ones(n, dtype=torch.float64, device="cuda")
+    assert float(torch.linalg.vector_norm(A.matvec(one))) <= 1e-11 * float(torch.linalg.vector_norm(A.values))
