@@ -249,6 +249,18 @@ def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
         out["csr_d2h"] = {"ms": d2h_ms, "bytes": nbytes, "gbs": nbytes / d2h_ms / 1e6,
                           "index_bytes": hi_.element_size()}
         del A, cold, hv, hi_, hp
+        # the coefficient planes' upload (a caller with host-side F), timed alone
+        hpl = torch.empty(planes.shape, dtype=planes.dtype, pin_memory=True)
+        hpl.copy_(planes)
+        dpl = torch.empty_like(planes)
+        torch.cuda.synchronize()
+        e0.record()
+        dpl.copy_(hpl, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        h2d_ms = e0.elapsed_time(e1)
+        out["planes_h2d"] = {"ms": h2d_ms, "bytes": hpl.numel() * 8, "gbs": hpl.numel() * 8 / h2d_ms / 1e6}
+        del hpl, dpl
     if cpu and rank == 0 and world == 1:
         from oracle import igs_oracle as O
 
