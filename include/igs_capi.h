@@ -102,8 +102,9 @@ enum {
   IGS_FLAG_DEFAULT = 0,
   IGS_FLAG_FORCE_GENERIC = 1,   /* use the stage-by-stage kernels even when a fused one applies */
   IGS_FLAG_ACCUMULATE = 2,      /* y += A x instead of y = A x (apply only)              */
-  IGS_FLAG_KERNEL_ONLY = 4      /* measurement: run only the fused apply's main kernel
-                                   (partial sums left in the workspace, y untouched)    */
+  IGS_FLAG_KERNEL_ONLY = 4      /* measurement: run only the fused main kernel (apply:
+                                   apply3d, y untouched; assembly: stage 1(+2), values
+                                   untouched) — the roofline's dominant kernel          */
 };
 
 /* ---- diagnostics ---------------------------------------------------- */

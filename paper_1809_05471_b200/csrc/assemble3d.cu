@@ -988,7 +988,8 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const ZRange
 
 template <int P, int Q>
 igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
-                   const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st) {
+                   const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st,
+                   bool kernel_only) {
   if (row_hi <= row_lo) return IGS_OK;
   ZRange z;
   IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
@@ -1000,6 +1001,7 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   if (tile == 4) IGS_TRY((launch3_stage12<P, Q, 4>(p, s, z, planes, H, st)));
   else if (tile == 2) IGS_TRY((launch3_stage12<P, Q, 2>(p, s, z, planes, H, st)));
   else if (tile == 1) IGS_TRY((launch3_stage12<P, Q, 1>(p, s, z, planes, H, st)));
+  if (kernel_only) return IGS_OK;  // measurement: the dominant kernel alone
   constexpr int W = 2 * P - 1;
   struct {
     int64_t NS0, NS1;
@@ -1087,7 +1089,8 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
 
 template <int P, int Q>
 igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
-                   const int64_t* base, const double* planes, double* values, double* G, cudaStream_t st) {
+                   const int64_t* base, const double* planes, double* values, double* G, cudaStream_t st,
+                   bool kernel_only) {
   constexpr int W = 2 * P - 1;
   switch (asm2_tile<P>(p->n_planes)) {
     case 8: IGS_TRY((launch2_stage1<P, Q, 8>(p, s, planes, G, st))); break;
@@ -1096,6 +1099,7 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
     case 1: IGS_TRY((launch2_stage1<P, Q, 1>(p, s, planes, G, st))); break;
     default: return fail(IGS_ECAPACITY, "2D assembly tile does not fit shared memory");
   }
+  if (kernel_only) return IGS_OK;  // measurement: the dominant kernel alone
   struct {
     int64_t NS0;
   } a{s.fs.nfn[0] * W};
@@ -1165,7 +1169,7 @@ size_t fused_assemble_workspace(const igs_problem* p, const Dims& D) {
 igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* const* rowptr1d,
                           const int64_t* const* cols1d, int64_t row_lo, int64_t row_hi,
                           const double* planes, double* values, void* ws, size_t ws_bytes,
-                          cudaStream_t st) {
+                          cudaStream_t st, int flags) {
   AsmShape s;
   if (!asm_shape(p, D, &s)) return fail(IGS_ECAPACITY, "no fused assembly");
   if (ws_bytes < asm_workspace(s) || !ws) return fail(IGS_EWORKSPACE, "workspace too small for the fused assembly");
@@ -1182,12 +1186,13 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
   row_start_kernel<<<1, 1, 0, st>>>(pat, row_lo, base);
   IGS_LAUNCH_CHECK("row_start_kernel");
   const int P = s.fs.p, Q = s.fs.k;
+  const bool ko = (flags & IGS_FLAG_KERNEL_ONLY) != 0;
   igs_status r = IGS_ECAPACITY;
   bool done = false;
 #define IGS_ASM_CASE(PP, QQ)                                                                    \
   if (!done && P == PP && Q == QQ) {                                                            \
-    r = p->d == 3 ? launch3<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st)   \
-                  : launch2<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st);  \
+    r = p->d == 3 ? launch3<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko)   \
+                  : launch2<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko);  \
     done = true;                                                                                \
   }
   IGS_ASM_CASE(2, 2)

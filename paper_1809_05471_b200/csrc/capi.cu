@@ -98,7 +98,7 @@ extern "C" igs_status igs_assemble_values(const igs_problem* prob, const int64_t
     if (!rowptr1d[k] || !cols1d[k]) return fail(IGS_EARG, "null 1D pattern");
   cudaStream_t s = as_stream(stream);
   if (!(flags & IGS_FLAG_FORCE_GENERIC) && block_eta < 0 && fused_assemble_supported(prob, D))
-    return fused_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, planes, values, ws, ws_bytes, s);
+    return fused_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, planes, values, ws, ws_bytes, s, flags);
   if (slab) return fail(IGS_ECAPACITY, "slab assembly needs the fused 3D kernels (uniform p = k, full sum)");
   return generic_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, block_eta, block_theta, planes,
                           values, ws, ws_bytes, s);

@@ -15,7 +15,7 @@ size_t fused_assemble_workspace(const igs_problem* p, const Dims& D);
 igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* const* rowptr1d,
                           const int64_t* const* cols1d, int64_t row_lo, int64_t row_hi,
                           const double* planes, double* values, void* ws, size_t ws_bytes,
-                          cudaStream_t s);
+                          cudaStream_t s, int flags = 0);
 
 // Shape class shared by the fused kernels: same spline order p in every
 // direction, trial == test, first-order derivative sets (0, e_1..e_d),
