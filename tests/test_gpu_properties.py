@@ -352,3 +352,16 @@ def test_layers_copy_kernel_and_single_rank_sharded_apply(cuda):
     y = torch.empty_like(x)
     sh.apply(x, y)
     assert torch.equal(y, op.apply_device(x, torch.empty_like(x)))
+
+
+def test_assembly_kernel_only_flag(cuda):
+    """IGS_FLAG_KERNEL_ONLY (measurement) runs the dominant assembly kernel
+    alone and returns; the next full assembly is unaffected."""
+    torch = cuda
+    *_, sumfac, matfree, workloads = _mods()
+    for d, p, K in [(3, 4, 6), (2, 5, 12)]:
+        prob = workloads.make_problem(d, p, K, 3 if d == 3 else 2, seed=8)
+        ref = sumfac.assemble(prob, flags=1).values_np()
+        sumfac.assemble(prob, flags=4)
+        torch.cuda.synchronize()
+        assert rel(sumfac.assemble(prob).values_np(), ref) <= 1e-12
