@@ -30,7 +30,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #ifdef IGS_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[8];
@@ -850,19 +853,55 @@ struct Tiling {
   int64_t box;
 };
 
+// Resident CTAs per SM of a fused apply configuration (occupancy query,
+// cached per kernel).
+int ctas_per_sm(const Launch& L) {
+  static std::mutex mu;
+  static std::map<void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find((void*)L.kernel);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaFuncSetAttribute(L.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, L.kernel, L.NT, L.smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache[(void*)L.kernel] = n;
+  return n;
+}
+
 Tiling tiling(const FusedShape& s, const Launch& L) {
   Tiling t;
   t.ntx = (int)ceil_div(s.nel[0], L.EX);
   t.nty = (int)ceil_div(s.nel[1], L.EY);
-  // z chunks: enough work items for ~8 waves of 2 CTAs per SM, chunks of at
-  // least P-1 layers so each DoF sees at most two chunks.
-  int K2 = (int)s.nel[2];
-  int64_t tiles = (int64_t)t.ntx * t.nty;
-  int want = (int)ceil_div(148 * 2 * 8, tiles);
-  int ez = (int)ceil_div(K2, want > 0 ? want : 1);
-  if (ez < s.p - 1) ez = s.p - 1;
-  if (ez < 1) ez = 1;
-  if (ez > K2) ez = K2;
+  // z chunks: as few as possible (each chunk costs a prologue and P-1 layers
+  // of overlapping partial sums) while the work items fill whole waves of
+  // resident CTAs (>= 97 % of the last wave); chunks of at least P-1 layers
+  // so each DoF sees at most two chunks.
+  const int K2 = (int)s.nel[2];
+  const int64_t tiles = (int64_t)t.ntx * t.nty;
+  const double slots = 148.0 * ctas_per_sm(L);
+  const int ez_min = s.p - 1 > 1 ? s.p - 1 : 1;
+  int best_ez = K2, pick_ez = 0;
+  double best_eff = -1.0;
+  for (int n = 1; n <= 16; ++n) {
+    int ez = (int)ceil_div(K2, n);
+    if (ez < ez_min) ez = ez_min;
+    if (ez > K2) ez = K2;
+    const int nch = (int)ceil_div(K2, ez);
+    const double w = nch * (double)tiles / slots;
+    const double eff = w / std::ceil(w);
+    if (eff >= 0.97) {
+      pick_ez = ez;
+      break;
+    }
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best_ez = ez;
+    }
+  }
+  const int ez = pick_ez ? pick_ez : best_ez;
   t.ez = ez;
   t.nch = (int)ceil_div(K2, ez);
   int FX = L.EX + s.p - 1, FY = L.EY + s.p - 1;
