@@ -22,6 +22,7 @@
 //         ring[m2][n2] += Σ_h W_z^{v2(h)} H_h  ->  CSR
 //   2D: asm2_stage1 (x) -> HBM, asm_sweep<2> (y ring, chunked) -> CSR.
 #include "fused.cuh"
+#include <cmath>
 #include <cstdlib>
 #include "tma.cuh"
 
@@ -971,9 +972,26 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const ZRange
   a.z1 = (int64_t)z.e_hi * Q;
   a.NE = z.e_hi - z.e_lo;
   a.zpl = (int64_t)z.sl * Q;
-  // z chunks: enough CTAs for ~4 waves at one CTA per SM
+  // z chunks: the fewest (each CTA refills its band tables) whose CTAs fill
+  // >= 97 % of the last wave at one CTA per SM (C3: 289 tiles -> 1 chunk)
   const int64_t tiles = (int64_t)a.nt0 * a.nt1;
-  int64_t nz = ceil_div(148 * 4, tiles);
+  int64_t nz = 1;
+  {
+    double best = -1.0;
+    for (int n = 1; n <= 16; ++n) {
+      const double w = n * (double)tiles / 148.0;
+      const double eff = w / std::ceil(w);
+      if (eff >= 0.97) {
+        nz = n;
+        break;
+      }
+      if (eff > best + 1e-9) {
+        best = eff;
+        nz = n;
+      }
+    }
+  }
+  if (nz > a.z1 - a.z0) nz = a.z1 - a.z0;
   if (nz < 1) nz = 1;
   a.lz = (int)ceil_div(a.z1 - a.z0, nz);
   if (a.lz < 1) a.lz = 1;
