@@ -901,7 +901,18 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
       best_ez = ez;
     }
   }
-  const int ez = pick_ez ? pick_ez : best_ez;
+  int ez = pick_ez ? pick_ez : best_ez;
+  {  // development switch for chunking experiments (IGS_APPLY_ZCHUNKS=n)
+    static const int forced = [] {
+      const char* e = getenv("IGS_APPLY_ZCHUNKS");
+      return e ? atoi(e) : 0;
+    }();
+    if (forced > 0) {
+      ez = (int)ceil_div(K2, forced);
+      if (ez < ez_min) ez = ez_min;
+      if (ez > K2) ez = K2;
+    }
+  }
   t.ez = ez;
   t.nch = (int)ceil_div(K2, ez);
   int FX = L.EX + s.p - 1, FY = L.EY + s.p - 1;
