@@ -1140,11 +1140,35 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   b.w2g = wlg;
   b.e_lo = 0;
   b.e_hi = K1;
-  // enough (slot, chunk) threads to fill the GPU, chunks >= 2(P-1) elements
-  int want = (int)ceil_div(148 * 1024, a.NS0);
-  int chunk = (int)ceil_div(K1, want > 0 ? want : 1);
-  if (chunk < 2 * (P - 1)) chunk = 2 * (P - 1);
-  if (chunk > K1) chunk = K1;
+  // chunks of >= 2(P-1) elements (each re-sweeps P-1 elements ahead of it):
+  // minimise waves x (chunk + P - 1), the waves counted against the sweep
+  // kernel's measured residency
+  int resident = 1;
+  {
+    constexpr size_t sm3 = S3Cfg<P, Q>::SMEM;
+    if (cudaFuncSetAttribute(asm_sweep<P, Q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm_sweep<P, Q, 2>, NT3, sm3) != cudaSuccess ||
+        resident < 1) {
+      cudaGetLastError();
+      resident = 1;
+    }
+  }
+  const int64_t slots = 148 * (int64_t)resident;
+  int chunk = K1;
+  {
+    int64_t best = -1;
+    for (int c = 2 * (P - 1); c <= K1; ++c) {
+      const int64_t blocks = nbsp * ceil_div(K1, c);
+      const int64_t cost = ceil_div(blocks, slots) * (c + P - 1);
+      if (best < 0 || cost < best) {
+        best = cost;
+        chunk = c;
+      }
+    }
+    if (chunk > K1) chunk = K1;
+    if (chunk < 1) chunk = 1;
+  }
   b.chunk = chunk;
   if (s.plan.ng > 4) return fail(IGS_ECAPACITY, "2D fused assembly sums at most 4 variant groups");
   b.ngrp = s.plan.ng;
