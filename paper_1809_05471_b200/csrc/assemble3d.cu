@@ -22,6 +22,7 @@
 //         ring[m2][n2] += Σ_h W_z^{v2(h)} H_h  ->  CSR
 //   2D: asm2_stage1 (x) -> HBM, asm_sweep<2> (y ring, chunked) -> CSR.
 #include "fused.cuh"
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include "tma.cuh"
@@ -1080,10 +1081,36 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
     const unsigned box[4] = {(unsigned)C::XR, (unsigned)A2_YS, 1u, (unsigned)p->n_planes};
     IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
   }
-  // y chunks: ~4 CTAs per SM in total, whole TMA boxes
-  const int64_t want = ceil_div(148 * 4, a.nt0);
-  int64_t yc = ceil_div(s.fs.npt[1], want > 0 ? want : 1);
-  yc = ceil_div(yc, A2_YS) * A2_YS;
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm2_stage1<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem),
+                     "smem attribute"));
+  // y chunks of whole TMA boxes: minimise waves x (boxes per CTA + 1 for the
+  // CTA's prologue), the waves counted against the measured residency
+  static std::atomic<int> res_cache[17];  // residency per plane count (the smem size), queried once
+  const int npl_key = p->n_planes < 0 ? 0 : (p->n_planes > 16 ? 16 : p->n_planes);
+  int resident = res_cache[npl_key].load(std::memory_order_relaxed);
+  if (resident <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm2_stage1<P, Q, T>, A2_NT, smem) !=
+            cudaSuccess ||
+        resident < 1) {
+      cudaGetLastError();
+      resident = 1;
+    }
+    res_cache[npl_key].store(resident, std::memory_order_relaxed);
+  }
+  const int64_t slots = 148 * (int64_t)resident, nbox = ceil_div(s.fs.npt[1], (int64_t)A2_YS);
+  int64_t yc = nbox * A2_YS;
+  {
+    int64_t best = -1;
+    for (int64_t per = 1; per <= nbox; ++per) {  // boxes per CTA
+      const int64_t ctas = a.nt0 * ceil_div(nbox, per);
+      const int64_t cost = ceil_div(ctas, slots) * (per + 1);
+      if (best < 0 || cost < best) {
+        best = cost;
+        yc = per * A2_YS;
+      }
+    }
+  }
   a.yc = (int)yc;
   const int64_t nyc = ceil_div(s.fs.npt[1], yc);
   // band tables after the G region and the last-direction element records
@@ -1092,14 +1119,11 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
                (((size_t)s.fs.nel[1] * S3Cfg<P, Q>::NWR + 1) & ~size_t(1));
   // GPU-filling grids share one table per tile (built once); small grids
   // (launch-bound, e.g. C1) fill it in the CTA and skip the extra launch
-  if (a.nt0 * nyc >= 2 * 148) {
+  if (nyc >= 4 && a.nt0 * nyc >= 2 * 148) {
     asm2_tables_kernel<P, Q, T><<<(unsigned)a.nt0, 256, 0, st>>>(a.tab, Wg);
     IGS_LAUNCH_CHECK("asm2_tables_kernel");
     a.Wg = Wg;
   }
-  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm2_stage1<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem),
-                     "smem attribute"));
   asm2_stage1<P, Q, T><<<(unsigned)(a.nt0 * nyc), A2_NT, smem, st>>>(a, fmap, p->n_planes);
   IGS_LAUNCH_CHECK("asm2_stage1");
   return IGS_OK;
@@ -1143,17 +1167,17 @@ igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   // chunks of >= 2(P-1) elements (each re-sweeps P-1 elements ahead of it):
   // minimise waves x (chunk + P - 1), the waves counted against the sweep
   // kernel's measured residency
-  int resident = 1;
-  {
+  static const int resident = [] {
     constexpr size_t sm3 = S3Cfg<P, Q>::SMEM;
+    int n = 1;
     if (cudaFuncSetAttribute(asm_sweep<P, Q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3) !=
             cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm_sweep<P, Q, 2>, NT3, sm3) != cudaSuccess ||
-        resident < 1) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, asm_sweep<P, Q, 2>, NT3, sm3) != cudaSuccess || n < 1) {
       cudaGetLastError();
-      resident = 1;
+      n = 1;
     }
-  }
+    return n;
+  }();
   const int64_t slots = 148 * (int64_t)resident;
   int chunk = K1;
   {
