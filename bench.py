@@ -297,6 +297,49 @@ def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
     return out
 
 
+def assembly_c2_section(reps=10, cpu=True, seed=0):
+    """C2 (BASELINE configs[1]: d=2, p=5, 256², stiffness) assembly, warm,
+    CUDA events; the CPU baseline is the oracle's Alg. 1 restatement on the
+    same full-size problem (one core)."""
+    import torch
+
+    from paper_1809_05471_b200 import sumfac, workloads
+
+    p, K = 5, 256
+    prob = workloads.make_problem(2, p, K, workloads.STIFF, seed=seed)
+    A = sumfac.assemble(prob)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        A = sumfac.assemble(prob)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    t = ms / 1e3
+    nnz = A.nnz
+    b_alg = 8 * prob.coeff.n_planes * prob.quad.num_points + 8 * nnz
+    f_ref = 2 * 460_800_000                   # the reference FlopCounter (SURVEY §8a a20)
+    peak_bw, _ = measured_peak()
+    out = {"workload": "C2", "desc": "d2 p5 256^2 stiffness assembly (warm, pattern cached)",
+           "value": nnz / t, "unit": "nnz/s", "ms": ms, "nnz": nnz, "fused": sumfac.fused_path(prob),
+           "roofline": {"bound": "latency (kernel-launch and per-CTA latency at this size)",
+                        "frac_ref_equivalent": f_ref / t / 37.15e12, "hbm_frac": b_alg / t / (peak_bw * 1e9),
+                        "alg_bytes": b_alg, "ref_flops": f_ref}}
+    if cpu:
+        from oracle import igs_oracle as O
+
+        sp = [O.uniform_space(p, K) for _ in range(2)]
+        planes = O.synthetic_planes(2, [p * K] * 2, 0, p * K, workloads.STIFF, seed)
+        ths = O.first_order_set(2)
+        t0 = time.perf_counter()
+        vals = O.assemble_sumfac(sp, sp, ths, ths, planes, O.plane_map(2, workloads.STIFF))
+        tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": vals.size / tc, "unit": "nnz/s", "cores": 1, "kind": "port",
+                               "sample": f"oracle Alg. 1 restatement, full C2 ({vals.size} nnz), {tc:.2f} s"}
+    return out
+
+
 def run_reference(args, w):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -461,6 +504,8 @@ def main():
     if not args.no_assembly:
         try:
             asm = assembly_section(cpu=not args.no_cpu_baseline, rank=rank, world=world)
+            if world == 1:
+                asm["c2"] = assembly_c2_section(cpu=not args.no_cpu_baseline)
         except Exception as exc:  # the apply line must still print
             asm = {"error": repr(exc)}
     if rank == 0:
