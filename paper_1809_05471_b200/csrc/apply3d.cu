@@ -745,17 +745,19 @@ struct ReduceArgs {
 };
 
 // y[n] = Σ over the work-item boxes covering n, in (tz, ty, tx) order.
-// Grid (x: n0 blocks, y: n1, z: n2 stride) — 32-bit coordinates, no 64-bit
-// divisions on the per-DoF path.
+// Grid (x: blocks over the flattened (n0, n1) layer — every lane busy even
+// when N0 is just past a multiple of 128 — y: n2 stride); 32-bit
+// coordinates, no 64-bit divisions on the per-DoF path.
 __global__ void __launch_bounds__(128) apply_reduce_kernel(const ReduceArgs r) {
-  const int n0 = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n0 >= r.N0) return;
+  const int n01 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int N0 = (int)r.N0;
+  if (n01 >= N0 * (int)r.N1) return;
+  const int n0 = n01 % N0, n1 = n01 / N0;
   const int EX = r.EX, EY = r.EY, FX = r.FX, FY = r.FY, ez = r.ez;
   const int tx_hi = min(r.ntx - 1, n0 / EX), tx_lo = n0 >= FX ? (n0 - FX) / EX + 1 : 0;
+  const int ty_hi = min(r.nty - 1, n1 / EY), ty_lo = n1 >= FY ? (n1 - FY) / EY + 1 : 0;
   const int zspan = ez + r.P - 1;
-  for (int n1 = blockIdx.y; n1 < r.N1; n1 += gridDim.y)
-  for (int n2 = blockIdx.z; n2 < r.N2; n2 += gridDim.z) {
-    const int ty_hi = min(r.nty - 1, n1 / EY), ty_lo = n1 >= FY ? (n1 - FY) / EY + 1 : 0;
+  for (int n2 = blockIdx.y; n2 < r.N2; n2 += gridDim.y) {
     const int tz_hi = min(r.nch - 1, n2 / ez), tz_lo = n2 >= zspan ? (n2 - zspan) / ez + 1 : 0;
     double s = 0.0;
     for (int tz = tz_lo; tz <= tz_hi; ++tz) {
@@ -1021,7 +1023,8 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
   r.ntx = t.ntx; r.nty = t.nty; r.nch = t.nch; r.ez = t.ez; r.K2 = (int)s.nel[2];
   r.box = t.box;
   r.accumulate = (flags & IGS_FLAG_ACCUMULATE) ? 1 : 0;
-  const dim3 rgrid((unsigned)ceil_div(r.N0, 128), (unsigned)min64(r.N1, 65535), (unsigned)min64(r.N2, 64));
+  if (r.N0 * r.N1 >= ((int64_t)1 << 31)) return fail(IGS_ECAPACITY, "DoF layer too large for the reduce");
+  const dim3 rgrid((unsigned)ceil_div(r.N0 * r.N1, 128), (unsigned)min64(r.N2, 64));
   apply_reduce_kernel<<<rgrid, 128, 0, st>>>(r);
   IGS_LAUNCH_CHECK("apply_reduce_kernel");
   return IGS_OK;
