@@ -102,9 +102,13 @@ enum {
   IGS_FLAG_DEFAULT = 0,
   IGS_FLAG_FORCE_GENERIC = 1,   /* use the stage-by-stage kernels even when a fused one applies */
   IGS_FLAG_ACCUMULATE = 2,      /* y += A x instead of y = A x (apply only)              */
-  IGS_FLAG_KERNEL_ONLY = 4      /* measurement: run only the fused main kernel (apply:
-                                   apply3d, y untouched; assembly: stage 1(+2), values
-                                   untouched) — the roofline's dominant kernel          */
+  IGS_FLAG_KERNEL_ONLY = 4,     /* measurement: run only the fused main kernel (apply:
+                                   apply3d, y untouched; two-pass assembly: stage 1(+2),
+                                   values untouched; the one-pass symmetric assembly is a
+                                   single kernel and runs whole) — the roofline's
+                                   dominant kernel                                       */
+  IGS_FLAG_TWO_PASS = 8         /* assembly: the two-kernel fused path (intermediate H in
+                                   HBM) even where the one-pass symmetric kernel applies */
 };
 
 /* ---- diagnostics ---------------------------------------------------- */

@@ -202,6 +202,28 @@ class BasisEvalTable:
         return out
 
 
+    def point_matrix(self, deriv=0):
+        """COO triplets (rows = point, cols = function, data) of the band,
+        structural zeros kept (bspline.py:287-297)."""
+        npts = self.num_points
+        rows = np.repeat(np.arange(npts), self.order)
+        cols = (self.first_active_np()[:, None] + np.arange(self.order)[None, :]).ravel()
+        data = self.values_np()[deriv].T.ravel()
+        return rows, cols, data
+
+    def restrict(self, point_slice, fn_lo, num_functions):
+        """View of this table on a point range and a function index range
+        (bspline.py:299-311); the device arrays are sliced, not copied."""
+        first = self.first_active[point_slice] - fn_lo
+        if first.numel():
+            lo, hi = int(first.min()), int(first.max())
+            if lo < 0 or hi + self.order > num_functions:
+                raise ValueError("restriction does not cover the active band")
+        return BasisEvalTable(self.order, num_functions, self.points[point_slice], self.max_deriv, first,
+                              self.values[:, :, point_slice],
+                              points_dev=None if self.points_dev is None else self.points_dev[point_slice])
+
+
 def tabulate(basis, points, max_deriv):
     """Evaluate the basis and derivatives 0..max_deriv at sorted points, on the GPU.
 

@@ -793,10 +793,14 @@ Launch make_launch() {
   return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG>};
 }
 
-// Measurement switch (IGS_APPLY_L2PF=-1, read once): every TMA box re-reads
-// the tile's first box (L2-resident), so the kernel runs without its HBM
-// stream — the compute-only time quoted in DESIGN.md §K4.  Results are wrong
-// in this mode; it is never set by the library.
+// Development switches, compiled only into the measurement build
+// (-DIGS_DEV_SWITCHES, tools/): IGS_APPLY_L2PF=-1 makes every TMA box re-read
+// the tile's first box (L2-resident) so the kernel runs without its HBM
+// stream (the compute-only time in DESIGN.md §K4; results are wrong in that
+// mode), IGS_APPLY_VARIANT picks alternative tile shapes and
+// IGS_APPLY_ZCHUNKS forces a z-chunk count.  The production library never
+// reads the environment.
+#ifdef IGS_DEV_SWITCHES
 int compute_only_mode() {
   static int v = 2;
   if (v == 2) {
@@ -805,8 +809,6 @@ int compute_only_mode() {
   }
   return v;
 }
-
-// Development switch (IGS_APPLY_VARIANT) for comparing tile shapes on the box.
 int apply_variant() {
   static int v = -1;
   if (v < 0) {
@@ -815,6 +817,18 @@ int apply_variant() {
   }
   return v;
 }
+int forced_zchunks() {
+  static const int forced = [] {
+    const char* e = getenv("IGS_APPLY_ZCHUNKS");
+    return e ? atoi(e) : 0;
+  }();
+  return forced;
+}
+#else
+constexpr int compute_only_mode() { return 0; }
+constexpr int apply_variant() { return 0; }
+constexpr int forced_zchunks() { return 0; }
+#endif
 
 // Tile shapes per order: EY·Q lines in groups of 8, Q2B point layers per
 // batch, one warp per (point layer, line group) of a batch.
@@ -904,11 +918,8 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
     }
   }
   int ez = pick_ez ? pick_ez : best_ez;
-  {  // development switch for chunking experiments (IGS_APPLY_ZCHUNKS=n)
-    static const int forced = [] {
-      const char* e = getenv("IGS_APPLY_ZCHUNKS");
-      return e ? atoi(e) : 0;
-    }();
+  {  // development switch for chunking experiments (measurement build only)
+    const int forced = forced_zchunks();
     if (forced > 0) {
       ez = (int)ceil_div(K2, forced);
       if (ez < ez_min) ez = ez_min;

@@ -911,6 +911,16 @@ TabArgs tab_args(const igs_problem* p) {
   return t;
 }
 
+#include "asm3_sym.cuh"
+
+// The one-pass symmetric kernel serves this problem (3D, p <= 4, A = Aᵀ).
+bool sym_eligible(const igs_problem* p, const AsmShape& s) {
+  // p = 3 keeps the two-pass path (measured faster: the 5-wide band does not
+  // fill the 8-wide MMA tiles of the one-pass kernel)
+  return s.fs.d == 3 && (s.fs.p == 2 || s.fs.p == 4) && problem_symmetric(p) &&
+         sym_fits_for(s.fs.p, s.plan, p->n_planes, s.fs.nfn[2]);
+}
+
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
   auto padded = [](int64_t n) { return (size_t)ceil_div(n, (int64_t)kSweepBlock) * kSweepBlock; };
@@ -1226,9 +1236,13 @@ bool fused_assemble_supported(const igs_problem* p, const Dims& D) {
   return asm_shape(p, D, &s);
 }
 
-size_t fused_assemble_workspace(const igs_problem* p, const Dims& D) {
+size_t fused_assemble_workspace(const igs_problem* p, const Dims& D, int flags) {
   AsmShape s;
   if (!asm_shape(p, D, &s)) return 0;
+  // whole-grid coefficients: the one-pass kernel covers every row range and
+  // needs only the row-offset scalar; a slab may need the two-kernel path
+  const bool slab = p->slab_lo || p->slab_hi;
+  if (!slab && !(flags & IGS_FLAG_TWO_PASS) && sym_eligible(p, s)) return 512;
   return asm_workspace(s);
 }
 
@@ -1238,7 +1252,7 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
                           cudaStream_t st, int flags) {
   AsmShape s;
   if (!asm_shape(p, D, &s)) return fail(IGS_ECAPACITY, "no fused assembly");
-  if (ws_bytes < asm_workspace(s) || !ws) return fail(IGS_EWORKSPACE, "workspace too small for the fused assembly");
+  if (ws_bytes < 512 || !ws) return fail(IGS_EWORKSPACE, "workspace too small for the fused assembly");
   TensorPat pat;
   pat.d = p->d;
   for (int k = 0; k < 3; ++k) {
@@ -1253,6 +1267,20 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
   IGS_LAUNCH_CHECK("row_start_kernel");
   const int P = s.fs.p, Q = s.fs.k;
   const bool ko = (flags & IGS_FLAG_KERNEL_ONLY) != 0;
+  if (row_hi <= row_lo) return IGS_OK;
+  if (sym_eligible(p, s) && !(flags & IGS_FLAG_TWO_PASS)) {
+    const bool slab = p->slab_lo || p->slab_hi;
+    const int sl = slab ? p->slab_lo : 0, sh = slab ? p->slab_hi : (int)s.fs.nel[2];
+    igs_status r = IGS_ECAPACITY;
+    switch (P) {
+      case 2: r = launch3_sym<2>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
+      case 3: r = launch3_sym<3>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
+      case 4: r = launch3_sym<4>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
+      default: break;
+    }
+    if (r != IGS_ECAPACITY) return r;  // else: the slab lacks the kernel's halo, two-pass below
+  }
+  if (ws_bytes < asm_workspace(s)) return fail(IGS_EWORKSPACE, "workspace too small for the fused assembly");
   igs_status r = IGS_ECAPACITY;
   bool done = false;
 #define IGS_ASM_CASE(PP, QQ)                                                                    \

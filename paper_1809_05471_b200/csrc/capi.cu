@@ -39,7 +39,7 @@ extern "C" size_t igs_workspace_bytes(const igs_problem* prob, int32_t op, int32
     case IGS_OP_EVAL_FIELD:
       return generic_eval_workspace(prob, D);
     case IGS_OP_ASSEMBLE:
-      if (!generic && fused_assemble_supported(prob, D)) return fused_assemble_workspace(prob, D);
+      if (!generic && fused_assemble_supported(prob, D)) return fused_assemble_workspace(prob, D, flags);
       return generic_assemble_workspace(prob, D);
     default:
       return 0;
@@ -53,7 +53,9 @@ extern "C" igs_status igs_apply(const igs_problem* prob, const double* planes, c
   if (!x || !y) return fail(IGS_EARG, "null vector");
   if (!planes && prob->n_planes > 0) return fail(IGS_EARG, "null coefficient planes");
   cudaStream_t s = as_stream(stream);
-  if (!(flags & IGS_FLAG_FORCE_GENERIC) && fused_apply_supported(prob, D))
+  // TMA needs 16-byte aligned planes: a misaligned view takes the generic kernels
+  const bool aligned = ((uintptr_t)planes & 15) == 0;
+  if (!(flags & IGS_FLAG_FORCE_GENERIC) && aligned && fused_apply_supported(prob, D))
     return fused_apply(prob, D, planes, x, y, ws, ws_bytes, flags, s);
   return generic_apply(prob, D, planes, x, y, ws, ws_bytes, flags, s);
 }
@@ -97,7 +99,8 @@ extern "C" igs_status igs_assemble_values(const igs_problem* prob, const int64_t
   for (int k = 0; k < prob->d; ++k)
     if (!rowptr1d[k] || !cols1d[k]) return fail(IGS_EARG, "null 1D pattern");
   cudaStream_t s = as_stream(stream);
-  if (!(flags & IGS_FLAG_FORCE_GENERIC) && block_eta < 0 && fused_assemble_supported(prob, D))
+  const bool aligned = ((uintptr_t)planes & 15) == 0;
+  if (!(flags & IGS_FLAG_FORCE_GENERIC) && block_eta < 0 && aligned && fused_assemble_supported(prob, D))
     return fused_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, planes, values, ws, ws_bytes, s, flags);
   if (slab) return fail(IGS_ECAPACITY, "slab assembly needs the fused 3D kernels (uniform p = k, full sum)");
   return generic_assemble(prob, D, rowptr1d, cols1d, row_lo, row_hi, block_eta, block_theta, planes,

@@ -11,7 +11,7 @@ igs_status fused_apply(const igs_problem* p, const Dims& D, const double* planes
                        double* y, void* ws, size_t ws_bytes, int flags, cudaStream_t s);
 
 bool fused_assemble_supported(const igs_problem* p, const Dims& D);
-size_t fused_assemble_workspace(const igs_problem* p, const Dims& D);
+size_t fused_assemble_workspace(const igs_problem* p, const Dims& D, int flags = 0);
 igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* const* rowptr1d,
                           const int64_t* const* cols1d, int64_t row_lo, int64_t row_hi,
                           const double* planes, double* values, void* ws, size_t ws_bytes,

@@ -113,7 +113,11 @@ class CoefficientField:
         self.eta_set = tuple(tuple(int(v) for v in t) for t in eta_set)
         if planes.device.type != "cuda" or planes.dtype != torch.float64 or planes.dim() != 2:
             raise ValueError("planes must be a float64 CUDA tensor [n_planes, npts]")
-        self.planes = planes if planes.stride(1) == 1 else planes.contiguous()
+        # the fused kernels read the planes by TMA (16-byte aligned base and
+        # plane stride): realign strided / offset views once here
+        if planes.stride(1) != 1 or planes.data_ptr() % 16 or (planes.shape[0] > 1 and planes.stride(0) % 2):
+            planes = planes.contiguous() if planes.stride(1) != 1 else planes.clone()
+        self.planes = planes
         self.plane_of = tuple(tuple(int(v) for v in r) for r in plane_of)
         if len(self.plane_of) != len(self.eta_set) or any(len(r) != len(self.theta_set) for r in self.plane_of):
             raise ValueError("plane_of must be [len(eta_set)][len(theta_set)]")
@@ -143,6 +147,16 @@ class CoefficientField:
 
     def is_zero_block(self, eta_idx, theta_idx):
         return self.plane_of[eta_idx][theta_idx] < 0
+
+    def restrict_flat(self, flat_idx, point_shape):
+        """Sub-field over a subset of grid points given as flat indices
+        (geometry.py:308-312); the planes are gathered on the device and the
+        plane map is kept."""
+        torch = _lib.require_cuda()
+        idx = torch.as_tensor(np.asarray(flat_idx, dtype=np.int64).reshape(-1), device=self.planes.device)
+        return CoefficientField.from_planes(self.theta_set, self.eta_set,
+                                            self.planes.index_select(1, idx).contiguous(),
+                                            self.plane_of, point_shape)
 
     @property
     def values(self):

@@ -14,8 +14,9 @@ group per step.  Each message is (p-1)·N0·N1 doubles.
 
 The assembly needs no communication (SlabAssembly): rank r owns the rows of
 DoF layers [lo_r, hi_r) of the last direction and reads the coefficients of
-elements [lo_r - p + 1, hi_r) — its slab plus a (p-1)-element halo — and
-writes its contiguous CSR slice; global indptr offsets are closed-form.
+elements [lo_r - 2(p-1), hi_r + p - 1) — its slab plus the halo the one-pass
+symmetric kernel needs for the mirrored half of its rows — and writes its
+contiguous CSR slice; global indptr offsets are closed-form.
 """
 
 import torch
@@ -175,9 +176,14 @@ class SlabAssembly:
         return self.part.own_layers(self.rank)
 
     def halo_elements(self):
-        """Elements whose coefficients the rank's rows need: [lo - p + 1, hi)."""
-        lo, hi = self.part.elements(self.rank)
-        return max(0, lo - self.part.p + 1), hi
+        """Elements whose coefficients the rank's rows need.  The rows of
+        DoF layers [a, b) sum elements [a - p + 1, b); the one-pass symmetric
+        kernel (csrc/asm3_sym.cuh) also forms the rows within p - 1 layers of
+        the block, whose mirrored entries land in it, so it reads elements
+        [a - 2(p - 1), b + p - 1) (clamped to the mesh)."""
+        a, b = self.own_layers()
+        p, K = self.part.p, self.part.K
+        return max(0, a - 2 * (p - 1)), min(K, b + p - 1)
 
     def row_range(self, layer_rows):
         a, b = self.own_layers()

@@ -242,6 +242,16 @@ class AssemblyProblem:
             self._cache["pattern"] = pat
         return pat
 
+    def core(self, dir_order=None):
+        """The assembly engine for one direction order (sumfac.py:325-337);
+        here a thin handle over the device kernels (see _DeviceCore)."""
+        key = ("core", tuple(dir_order) if dir_order is not None else None)
+        core = self._cache.get(key)
+        if core is None:
+            core = _DeviceCore(self, dir_order)
+            self._cache[key] = core
+        return core
+
     def struct(self, dir_order=None, slab=None, with_pattern=True):
         """The C igs_problem for this problem (cached per dir_order/slab)."""
         key = ("struct", tuple(dir_order) if dir_order is not None else None,
@@ -256,6 +266,34 @@ class AssemblyProblem:
                                  slab=slab)
             self._cache[key] = hit
         return hit
+
+
+class _DeviceCore:
+    """Device counterpart of the reference's _Core (sumfac.py:143-229): the
+    tables, pattern and direction order are fixed by the problem; values
+    come back in CSR order from igs_assemble_values."""
+
+    def __init__(self, problem, dir_order=None):
+        d = problem.d
+        self.problem = problem
+        self.dir_order = tuple(dir_order) if dir_order is not None else tuple(range(d))
+        if sorted(self.dir_order) != list(range(d)):
+            raise ValueError("dir_order must be a permutation of the directions")
+        self.pattern = problem.pattern()
+        self.d = d
+
+    def assemble_values(self, counter=None):
+        """CSR-ordered values of the summed non-zero blocks (device tensor)."""
+        return _run_assembly(self.problem, None, counter, self.dir_order)
+
+    def block_values_csr(self, theta, eta, counter=None):
+        """One derivative block's values in CSR order (device tensor)."""
+        theta, eta = _check_block_indices(self.problem, theta, eta)
+        i, j = self.problem.eta_set.index(eta), self.problem.theta_set.index(theta)
+        torch = _lib.require_cuda()
+        if self.problem.coeff_field().is_zero_block(i, j) or self.pattern.nnz == 0:
+            return torch.zeros(self.pattern.nnz, dtype=torch.float64, device="cuda")
+        return _run_assembly(self.problem, (i, j), counter, self.dir_order)
 
 
 def _tabulate(basis, points, max_deriv):

@@ -177,6 +177,27 @@ class SparsityPattern:
             self._host["indices"] = self.indices_dev.cpu().numpy().astype(np.int64, copy=False)
         return self._host["indices"]
 
+    def value_perm(self, dir_order):
+        """Permutation from the assembly-value layout (pair index of the
+        first processed direction fastest) into CSR value order
+        (tensorspace.py:324-332): CSR position k holds layout entry perm[k].
+        Host numpy, cached per dir_order; the device kernels write CSR order
+        directly and never need it."""
+        dir_order = tuple(int(v) for v in dir_order)
+        key = ("vperm", dir_order)
+        if key not in self._host:
+            d = self.d
+            # layout axes, slowest first: the last processed direction first
+            m_flat = np.zeros(1, dtype=np.int64)
+            n_flat = np.zeros(1, dtype=np.int64)
+            for delta in reversed(dir_order):
+                dp = self.dir_pairs[delta]
+                m_flat = (m_flat[:, None] + dp.m[None, :] * self.test_ordering.strides[delta]).ravel()
+                n_flat = (n_flat[:, None] + dp.n[None, :] * self.trial_ordering.strides[delta]).ravel()
+            del d
+            self._host[key] = np.lexsort((n_flat, m_flat))
+        return self._host[key]
+
     def to_scipy(self, values=None):
         import scipy.sparse
 

@@ -265,8 +265,8 @@ def test_slab_assembly_matches_full(cuda, p, K, kind, world):
     # a row range needing elements outside the slab is rejected
     sa = SlabAssembly(part, world - 1)
     lo, hi = sa.halo_elements()
-    planes = full_planes[:, (lo + 1) * p * layer_pts: hi * p * layer_pts].contiguous()
-    field = workloads.field_from_planes(3, kind, planes, quad.shape, slab=(lo + 1, hi))
+    planes = full_planes[:, lo * p * layer_pts: (hi - 1) * p * layer_pts].contiguous()
+    field = workloads.field_from_planes(3, kind, planes, quad.shape, slab=(lo, hi - 1))
     with pytest.raises(ValueError):
         sa.assemble(AssemblyProblem(bases, bases, quad, field))
     del torch

@@ -91,6 +91,17 @@ def test_localized_assembly_and_apply_equal_global(cuda, d, p, K, kind, strategy
     yl = localized.apply_localized(prob, part, x)
     assert float(torch.linalg.vector_norm(yl - y) / torch.linalg.vector_norm(y)) <= 1e-12
     assert float(torch.linalg.vector_norm(localized.apply_localized(prob, part, torch.zeros_like(x)))) == 0.0
+    # counted MACs: the sum of the per-box applies' counts
+    from paper_1809_05471_b200.localized import restrict, _local_field
+
+    c = sumfac.FlopCounter()
+    localized.apply_localized(prob, part, x, counter=c)
+    want = sumfac.FlopCounter()
+    for i in range(len(part)):
+        ls = restrict(prob.trial, prob.test, prob.quad, part, i)
+        matfree.MatrixFreeOperator(sumfac.AssemblyProblem(ls.trial, ls.test, ls.quad,
+                                                          _local_field(prob, ls))).count(want)
+    assert c == want and c.total > 0
 
 
 @pytest.mark.gpu

@@ -19,10 +19,12 @@ def test_assembly_row_blocks_partition_rows_and_halo_covers_support(K, p, world)
         assert (lo, hi) == (a * layer_rows, b * layer_rows)
         covered.append((a, b))
         e_lo, e_hi = sa.halo_elements()
-        # rows of DoF layer m are sums over elements [m - p + 1, m] ∩ [0, K)
-        need_lo, need_hi = max(0, a - p + 1), min(K, b)
-        assert e_lo <= need_lo and e_hi >= need_hi
-        assert e_hi - e_lo <= (part.elements(r)[1] - part.elements(r)[0]) + p - 1
+        # rows of DoF layer m are sums over elements [m - p + 1, m] ∩ [0, K);
+        # the one-pass symmetric kernel also forms the rows whose mirrored
+        # entries land in the block: layers [a - p + 1, b + p - 1)
+        need_lo, need_hi = max(0, a - 2 * (p - 1)), min(K, b + p - 1)
+        assert (e_lo, e_hi) == (need_lo, need_hi)
+        assert e_hi - e_lo <= (part.elements(r)[1] - part.elements(r)[0]) + 4 * (p - 1)
     assert covered[0][0] == 0 and covered[-1][1] == n_layers
     for (a0, b0), (a1, b1) in zip(covered, covered[1:]):
         assert b0 == a1 and a1 >= a0
