@@ -90,8 +90,8 @@ struct SymCfg {
   // + z-row table: 3 int64 per DoF row of the chunk's sweep (zrows rows)
   static constexpr int NPEND = (P - 1) * (2 * P - 2) - (P - 1) * (P - 2) / 2;  // pending z values per pair
   static constexpr size_t smem(int npl, int ng, int zrows = 0) {
-    return (fbuf(npl) + (size_t)ng * XRP1 * SPG + W0C + W1C + HS + 2 * FZ + (size_t)NPEND * NPAIR +
-            3 * (size_t)zrows) * sizeof(double) + 32;
+    return (fbuf(npl) + 2 * (size_t)ng * XRP1 * SPG + W0C + W1C + 2 * HS + 2 * FZ + 3 * (size_t)zrows) *
+               sizeof(double) + 32;
   }
   static_assert(XR1 <= 256 && XB0 <= 256, "TMA box");
   static_assert(NPAIR <= NT, "one pair per thread");
@@ -258,6 +258,33 @@ struct Pend {
     }                                                                                        \
   } while (0)
 
+// TMEM (tcgen05) helpers: the pending z rows live in tensor memory, one
+// private 32-column slice of its lane per thread (warp w owns lanes
+// 32·(w % 4) .. +31; warps w, w+4, w+8, w+12 take column groups 0..3).
+// issue only: tcgen05.wait::ld before the registers are used
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // the previous store has landed
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+__device__ __forceinline__ double u2d(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
+
 template <int P, int T0, int T1>
 __global__ void __launch_bounds__(512, 1)
     asm3_sym(const SymArgs a, const __grid_constant__ CUtensorMap fmap) {
@@ -266,20 +293,21 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int Q = C::Q, W = C::W, NS0 = C::NS0, NST0 = C::NST0, SR1 = C::SR1, NMT1 = C::NMT1;
   constexpr int XB0 = C::XB0, XR1 = C::XR1, XRP1 = C::XRP1, NYT = C::NYT, SPG = C::SPG, HP = C::HP;
   constexpr int KS0 = C::KS0, W0R = C::W0R, KS1 = C::KS1, W1P = C::W1P, PP = C::PP, FZ = C::FZ;
-  constexpr int NT = C::NT, NW = C::NW, NPAIR = C::NPAIR;
+  constexpr int NT = C::NT, NW = C::NW, NPAIR = C::NPAIR, NPW = (NPAIR + 31) / 32;
+  static_assert(2 * PD::N <= 32, "pending rows fit a 32-column TMEM slice");
   extern __shared__ __align__(128) double sm[];
-  const AsmPlan& pl = a.plan;
-  const int ng = pl.ng;
+  const int ng = a.plan.ng;
   const size_t fb = C::fbuf(a.nplanes);
+  const size_t gsz = (size_t)ng * XRP1 * SPG;
   double* Fs = sm;                                   // [npl][XR1][XB0] (+ zero tail)
-  double* Gs = Fs + fb;                              // [ng][XRP1][SPG]
-  double* W0 = Gs + (size_t)ng * XRP1 * SPG;         // [4][NST0][KS0·4][W0R]
+  double* Gs = Fs + fb;                              // [2][ng][XRP1][SPG]
+  double* W0 = Gs + 2 * gsz;                         // [4][NST0][KS0·4][W0R]
   double* W1 = W0 + C::W0C;                          // [4][NMT1][8][W1P]
-  double* Hs = W1 + C::W1C;                          // [4][NS1C][HP]
-  double* FZs = Hs + C::HS;                          // [2][FZ]
-  double* PS = FZs + 2 * FZ;                         // [PD::N][NPAIR] pending z rows
-  int64_t* ZR = reinterpret_cast<int64_t*>(PS + (size_t)PD::N * NPAIR);  // [zrows][3]
+  double* Hs = W1 + C::W1C;                          // [2][4][NS1C][HP]
+  double* FZs = Hs + 2 * C::HS;                      // [2][FZ]
+  int64_t* ZR = reinterpret_cast<int64_t*>(FZs + 2 * FZ);  // [zrows][3]
   uint64_t* bar = reinterpret_cast<uint64_t*>(ZR + 3 * (size_t)a.zrows);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, m4 = lane & 3;
   const int t0 = blockIdx.x % a.nt0, t1 = blockIdx.x / a.nt0;
@@ -294,19 +322,26 @@ __global__ void __launch_bounds__(512, 1)
   const int64_t N0 = a.tab.N[0], N1 = a.tab.N[1], N2 = a.tab.N[2];
   const int64_t layer = N0 * N1;
   const unsigned fbytes = (unsigned)((size_t)a.nplanes * XR1 * XB0 * sizeof(double));
+  const int nz = (e_hi - e_lo) * Q;
 
-  // ---- prologue: zero shared memory, tables, barrier, first layer -----------
-  for (size_t i = tid; i < fb + (size_t)ng * XRP1 * SPG; i += NT) sm[i] = 0.0;
-  for (int i = tid; i < PD::N * NPAIR; i += NT) PS[i] = 0.0;
-  for (int i = tid; i < (int)C::HS; i += NT) Hs[i] = 0.0;
+  // ---- prologue: TMEM, zeroed shared memory, tables, barrier, first layer ---
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(
+                     dev::smem_u32(tmem_holder)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  for (size_t i = tid; i < fb + 2 * gsz; i += NT) sm[i] = 0.0;
+  for (int i = tid; i < 2 * (int)C::HS; i += NT) Hs[i] = 0.0;
   if (tid == 0) {
     dev::mbar_init(bar, 1);
     dev::fence_mbar_init();
   }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t taddr = *tmem_holder + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
   dev::fence_proxy_async();
   __syncthreads();
-  const int nz = (e_hi - e_lo) * Q;
   if (tid == 0 && nz > 0) {
     dev::mbar_expect_tx(bar, fbytes);
     dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)((int64_t)e_lo * Q - a.zpl), 0);
@@ -314,6 +349,13 @@ __global__ void __launch_bounds__(512, 1)
   sym_fill_table<P, T0, T1, false>(W0, a.tab, 0, a0, xb0);
   sym_fill_table<P, T0, T1, true>(W1, a.tab, 1, a1, xb1);
   if (e_lo < e_hi) sym_fill_fz<P>(FZs, a.tab, e_lo, tid, NT);
+  if (warp < NPW) {  // pending rows start at zero
+    uint32_t z[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) z[i] = 0u;
+    tmem_st32(taddr, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
 
   // ---- this thread's (s0, s1) pair and its CSR addressing ------------------
   const int s0 = tid % NS0, s1c = tid / NS0;
@@ -376,79 +418,161 @@ __global__ void __launch_bounds__(512, 1)
   for (int i = 0; i < P; ++i)
 #pragma unroll
     for (int j = 0; j < P; ++j) E[i][j] = 0.0;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 
-  // stage-1 tasks: (y tile, n-tile, half of the blocks)
+  // stage-1 tasks: (y tile, n-tile, half of the blocks); warp w runs on SMSP
+  // w % 4, so each SMSP gets one y tile's tasks
   const int nt1 = 2 * NYT * NST0;
-  // stage-2 task: (m-tile, n-tile, half of the stage-2 groups); halves
-  // alternate across SMSPs (warp w runs on SMSP w % 4) so each SMSP gets both
+  // stage-2 tasks: (m-tile, n-tile, half of the stage-2 groups); halves
+  // alternate across SMSPs so each SMSP gets both
   const int nt2 = NMT1 * NST0 * 2;
   unsigned ph = 0u;
   double fzr[C::FZL];
-  for (int e = e_lo; e < e_hi; ++e) {
-    const double* fzb = FZs + ((e - e_lo) & 1) * FZ;
+
+  // stage 1 of point layer iz (F in smem) into G buffer gb
+  auto stage1 = [&](double* Gb) {
+    for (int t = warp; t < nt1; t += NW) {
+      const int yt = t % NYT, st = (t / NYT) % NST0, half = t / (NYT * NST0);
+      const int b_lo = half ? a.plan.half_b : 0, b_hi = half ? a.plan.nb : a.plan.half_b;
+      int klo = 0;
+#pragma unroll
+      for (int i = 0; i < NST0; ++i)
+        if (i == st) klo = C::k0_lo(i);
+      const double* Fy = Fs + (yt * 8 + g8) * XB0 + m4 + klo * 4;
+      const double* Wk = W0 + (st * KS0 * 4 + m4) * W0R + g8;
+      double* Gy = Gb + (yt * 8 + g8) * SPG + st * 8 + 2 * m4;
+      const bool st_ok = st * 8 + 2 * m4 < NS0;
+      double c0 = 0.0, c1 = 0.0;
 #pragma unroll 1
-    for (int q = 0; q < Q; ++q) {
-      const int iz = (e - e_lo) * Q + q;
-      if (q == 0 && e + 1 < e_hi && warp == NW - 1) {
+      for (int b = b_lo; b < b_hi; ++b) {
+        const double* Fp = Fy + a.b_plane[b] * (XR1 * XB0);
+        const double* Wv = Wk + a.b_v0[b] * (NST0 * KS0 * 4 * W0R);
+        double f[KS0], w[KS0];
 #pragma unroll
-        for (int i = 0; i < C::FZL; ++i) fzr[i] = sym_fz_value<P>(a.tab, e + 1, lane + 32 * i);
-      }
-      dev::mbar_wait(bar, ph);
-      ph ^= 1u;
-      // ---- stage 1 ------------------------------------------------------------
-      // task = (y tile, n-tile, half of the blocks): every warp, one chain;
-      // warp w runs on SMSP w % 4, so each SMSP gets one y tile's 4 tasks
-      for (int t = warp; t < nt1; t += NW) {
-        const int yt = t % NYT, st = (t / NYT) % NST0, half = t / (NYT * NST0);
-        const int b_lo = half ? pl.half_b : 0, b_hi = half ? pl.nb : pl.half_b;
-        int klo = 0;
+        for (int kk = 0; kk < KS0; ++kk) {
+          f[kk] = Fp[kk * 4];
+          w[kk] = Wv[kk * 4 * W0R];
+        }
 #pragma unroll
-        for (int i = 0; i < NST0; ++i)
-          if (i == st) klo = C::k0_lo(i);
-        const double* Fy = Fs + (yt * 8 + g8) * XB0 + m4 + klo * 4;
-        const double* Wk = W0 + (st * KS0 * 4 + m4) * W0R + g8;
-        // two accumulator chains (even / odd k-steps), summed at the group end
-        double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-        double* Gy = Gs + (yt * 8 + g8) * SPG + st * 8 + 2 * m4;
-        const bool st_ok = st * 8 + 2 * m4 < NS0;
-#pragma unroll 1
-        for (int b = b_lo; b < b_hi; ++b) {
-          const double* Fp = Fy + a.b_plane[b] * (XR1 * XB0);
-          const double* Wv = Wk + a.b_v0[b] * (NST0 * KS0 * 4 * W0R);
-          double f[KS0], w[KS0];
-#pragma unroll
-          for (int kk = 0; kk < KS0; ++kk) {
-            f[kk] = Fp[kk * 4];
-            w[kk] = Wv[kk * 4 * W0R];
-          }
-#pragma unroll
-          for (int kk = 0; kk < KS0; ++kk) {
-            if (kk & 1) dmma_a(e0, e1, f[kk], w[kk]);
-            else dmma_a(c0, c1, f[kk], w[kk]);
-          }
-          if ((a.b_end >> b) & 1) {
-            if (st_ok) *reinterpret_cast<double2*>(Gy + a.b_g[b] * (XRP1 * SPG)) = make_double2(c0 + e0, c1 + e1);
-            c0 = c1 = e0 = e1 = 0.0;
-          }
+        for (int kk = 0; kk < KS0; ++kk) dmma_a(c0, c1, f[kk], w[kk]);
+        if ((a.b_end >> b) & 1) {
+          if (st_ok) *reinterpret_cast<double2*>(Gy + a.b_g[b] * (XRP1 * SPG)) = make_double2(c0, c1);
+          c0 = c1 = 0.0;
         }
       }
-      __syncthreads();
-      // F is consumed: fetch the next layer while stages 2 and 3 run
-      if (tid == 0 && iz + 1 < nz) {
-        dev::fence_proxy_async();
-        dev::mbar_expect_tx(bar, fbytes);
-        dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)((int64_t)e_lo * Q + iz + 1 - a.zpl), 0);
-      }
-      // next element's z factors: loaded into registers at q = 0, stored at
-      // q = 1 (the other buffer was last read in element e - 1)
-      if (q == 1 && e + 1 < e_hi && warp == NW - 1) {
-        double* dst = FZs + ((e + 1 - e_lo) & 1) * FZ;
+    }
+  };
+  if (nz > 0) {
+    dev::mbar_wait(bar, ph);
+    ph ^= 1u;
+    stage1(Gs);
+  }
+  __syncthreads();
+  if (tid == 0 && nz > 1) {
+    dev::fence_proxy_async();
+    dev::mbar_expect_tx(bar, fbytes);
+    dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)((int64_t)e_lo * Q + 1 - a.zpl), 0);
+  }
+
+  // stage 3 of layer k-1: this thread's pair, point layer -> E; element end
+  // -> row out, pending rows (TMEM) updated
+  auto stage3 = [&](int k) {
+    if (k >= 1 && warp < NPW) {
+      const int z = k - 1, es = e_lo + z / Q, qs = z % Q;
+      const double* fq = FZs + ((es - e_lo) & 1) * FZ + qs * 4 * PP;
+      const double* hcol = Hs + (z & 1) * C::HS + s1c * HP + s0;
+      double hv[4];
 #pragma unroll
-        for (int i = 0; i < C::FZL; ++i)
-          if (lane + 32 * i < FZ) dst[lane + 32 * i] = fzr[i];
+      for (int v = 0; v < 4; ++v) hv[v] = a.vmap[v] >= 0 ? hcol[a.vmap[v] * (C::NS1C * HP)] : 0.0;
+      double fbv[4][P];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int j = 0; j < P; j += 2) {
+          if (j + 1 < P) {
+            const double2 tt = *reinterpret_cast<const double2*>(fq + f * PP + j);
+            fbv[f][j] = tt.x;
+            fbv[f][j + 1] = tt.y;
+          } else {
+            fbv[f][j] = fq[f * PP + j];
+          }
+        }
+      // Σ_{θ,η} (w·B^θ_jn)(B^η_jm) H_{θ+2η}: θ first (u_η[jn]), then η
+      double u0[P], u1[P];
+#pragma unroll
+      for (int jn = 0; jn < P; ++jn) {
+        u0[jn] = fma(fbv[1][jn], hv[1], fbv[0][jn] * hv[0]);
+        u1[jn] = fma(fbv[1][jn], hv[3], fbv[0][jn] * hv[2]);
       }
-      // ---- stage 2 ------------------------------------------------------------
+#pragma unroll
+      for (int jm = 0; jm < P; ++jm)
+#pragma unroll
+        for (int jn = 0; jn < P; ++jn) E[jm][jn] = fma(fbv[3][jm], u1[jn], fma(fbv[2][jm], u0[jn], E[jm][jn]));
+      if (qs == Q - 1) {
+        // element es done: row es is final; the pending rows move up one age
+        uint32_t rr[32];
+        tmem_ld32(taddr, rr);
+        tmem_wait_ld();
+        double row[W];
+#pragma unroll
+        for (int kx = 0; kx < W; ++kx) {
+          double v = kx < PD::len(0) ? u2d(rr[2 * (PD::off(0) + kx)], rr[2 * (PD::off(0) + kx) + 1]) : 0.0;
+          if (kx >= P - 1) v += E[0][kx - (P - 1)];
+          row[kx] = v;
+        }
+        // age ag <- age ag+1 + E[ag+1] (row es+1+ag, kx = jn + P - 2 - ag)
+#pragma unroll
+        for (int ag = 0; ag < P - 1; ++ag) {
+#pragma unroll
+          for (int kx = 0; kx < PD::len(ag); ++kx) {
+            const int src = PD::off(ag + 1) + kx;
+            double v = (ag + 1 < P - 1 && kx < PD::len(ag + 1)) ? u2d(rr[2 * src], rr[2 * src + 1]) : 0.0;
+            const int jn = kx - (P - 2 - ag);
+            if (jn >= 0 && jn < P) v += E[ag + 1][jn];
+            const int dst = PD::off(ag) + kx;
+            rr[2 * dst] = (uint32_t)__double2loint(v);
+            rr[2 * dst + 1] = (uint32_t)__double2hiint(v);
+          }
+        }
+        tmem_st32(taddr, rr);
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+#pragma unroll
+          for (int j = 0; j < P; ++j) E[i][j] = 0.0;
+        IGS_SYM_STORE(es, row);
+      }
+    }
+  };
+
+  // ---- one phase per point layer k: stage 3 of k-1, stage 2 of k, stage 1
+  // of k+1 (G, H double-buffered), one barrier --------------------------------
+#pragma unroll 1
+  for (int k = 0; k <= nz; ++k) {
+    // ---- stage 3 of layer k-1 ------------------------------------------------
+    stage3(k);
+    // next element's z factors: loaded at the first layer of an element (in
+    // stage 3 terms), stored one phase later (the other buffer's last reader,
+    // the previous element's stage 3, finished two barriers before)
+    if (warp == NW - 1 && k >= 1) {
+      const int z = k - 1, es = e_lo + z / Q, qs = z % Q;
+      if (es + 1 < e_hi) {
+        if (qs == 0) {
+#pragma unroll
+          for (int i = 0; i < C::FZL; ++i) fzr[i] = sym_fz_value<P>(a.tab, es + 1, lane + 32 * i);
+        } else if (qs == 1) {
+          double* dst = FZs + ((es + 1 - e_lo) & 1) * FZ;
+#pragma unroll
+          for (int i = 0; i < C::FZL; ++i)
+            if (lane + 32 * i < FZ) dst[lane + 32 * i] = fzr[i];
+        }
+      }
+    }
+    // ---- stage 2 of layer k: G[k&1] -> H[k&1] ---------------------------------
+    if (k < nz) {
+      const double* Gb = Gs + (k & 1) * gsz;
+      double* Hb = Hs + (k & 1) * C::HS;
       for (int t = warp; t < nt2; t += NW) {
         const bool by8 = nt2 % 8 == 0;
         const int hh = by8 ? (t >> 2) & 1 : t & 1;
@@ -457,18 +581,16 @@ __global__ void __launch_bounds__(512, 1)
         const int g_lo = hh ? a.hsplit : 0, g_hi = hh ? ng : a.hsplit;
         const int s1 = mt * 8 + g8;
         const int rr1 = s1 / SR1, oo1 = s1 % SR1;
-        const bool row_ok = rr1 < T1 && oo1 < W;
         const int sc = 8 * st + 2 * m4;
-        double* Hd = Hs + (rr1 * W + oo1) * HP + sc;
+        const bool h_ok = rr1 < T1 && oo1 < W && sc < NS0;
+        double* Hd = Hb + (rr1 * W + oo1) * HP + sc;
         const double* Wk = W1 + (mt * 8 + g8) * W1P + m4;
-        double d0 = 0.0, d1 = 0.0;
         int klo = 0;
 #pragma unroll
         for (int i = 0; i < NMT1; ++i)
           if (i == mt) klo = C::k1_lo(i);
-        const double* Gk = Gs + (klo * 4 + m4) * SPG + 8 * st + g8;
-        const bool h_ok = row_ok && sc < NS0;
-        double e0 = 0.0, e1 = 0.0;
+        const double* Gk = Gb + (klo * 4 + m4) * SPG + 8 * st + g8;
+        double d0 = 0.0, d1 = 0.0;
 #pragma unroll 1
         for (int g = g_lo; g < g_hi; ++g) {
           const double* Wg = Wk + a.g_v1[g] * (NMT1 * 8 * W1P);
@@ -480,88 +602,47 @@ __global__ void __launch_bounds__(512, 1)
             gv[kk] = Gg[kk * 4 * SPG];
           }
 #pragma unroll
-          for (int kk = 0; kk < KS1; ++kk) {
-            if (kk & 1) dmma_a(e0, e1, wv[kk], gv[kk]);
-            else dmma_a(d0, d1, wv[kk], gv[kk]);
-          }
+          for (int kk = 0; kk < KS1; ++kk) dmma_a(d0, d1, wv[kk], gv[kk]);
           if ((a.g_end >> g) & 1) {
-            if (h_ok) *reinterpret_cast<double2*>(Hd + a.g_h[g] * (C::NS1C * HP)) = make_double2(d0 + e0, d1 + e1);
-            d0 = d1 = e0 = e1 = 0.0;
+            if (h_ok) *reinterpret_cast<double2*>(Hd + a.g_h[g] * (C::NS1C * HP)) = make_double2(d0, d1);
+            d0 = d1 = 0.0;
           }
         }
-      }
-      __syncthreads();
-      // ---- stage 3: this point layer's z contraction into E -------------------
-      if (tid < NPAIR) {
-        const double* hcol = Hs + s1c * HP + s0;
-        double hv[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) hv[v] = a.vmap[v] >= 0 ? hcol[a.vmap[v] * (C::NS1C * HP)] : 0.0;
-        const double* fq = fzb + q * 4 * PP;
-        double fbv[4][P];
-#pragma unroll
-        for (int f = 0; f < 4; ++f)
-#pragma unroll
-          for (int j = 0; j < P; j += 2) {
-            if (j + 1 < P) {
-              const double2 tt = *reinterpret_cast<const double2*>(fq + f * PP + j);
-              fbv[f][j] = tt.x;
-              fbv[f][j + 1] = tt.y;
-            } else {
-              fbv[f][j] = fq[f * PP + j];
-            }
-          }
-        // Σ_{θ,η} (w·B^θ_jn)(B^η_jm) H_{θ+2η}: θ first (u_η[jn]), then η
-        double u0[P], u1[P];
-#pragma unroll
-        for (int jn = 0; jn < P; ++jn) {
-          u0[jn] = fma(fbv[1][jn], hv[1], fbv[0][jn] * hv[0]);
-          u1[jn] = fma(fbv[1][jn], hv[3], fbv[0][jn] * hv[2]);
-        }
-#pragma unroll
-        for (int jm = 0; jm < P; ++jm)
-#pragma unroll
-          for (int jn = 0; jn < P; ++jn) E[jm][jn] = fma(fbv[3][jm], u1[jn], fma(fbv[2][jm], u0[jn], E[jm][jn]));
       }
     }
-    // ---- element e done: row e is final; the pending rows move up one age --
-    if (tid < NPAIR) {
-      double* ps = PS + tid;
-      double row[W];
-#pragma unroll
-      for (int k = 0; k < W; ++k) {
-        double v = k < PD::len(0) ? ps[(PD::off(0) + k) * NPAIR] : 0.0;
-        if (k >= P - 1) v += E[0][k - (P - 1)];
-        row[k] = v;
-      }
-      // age a <- age a+1 + E[a+1] (row e+1+a, k = jn + P - 2 - a)
-#pragma unroll
-      for (int ag = 0; ag < P - 1; ++ag) {
-#pragma unroll
-        for (int k = 0; k < PD::len(ag); ++k) {
-          double v = (ag + 1 < P - 1 && k < PD::len(ag + 1)) ? ps[(PD::off(ag + 1) + k) * NPAIR] : 0.0;
-          const int jn = k - (P - 2 - ag);
-          if (jn >= 0 && jn < P) v += E[ag + 1][jn];
-          ps[(PD::off(ag) + k) * NPAIR] = v;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < P; ++i)
-#pragma unroll
-        for (int j = 0; j < P; ++j) E[i][j] = 0.0;
-      IGS_SYM_STORE(e, row);
+    // ---- stage 1 of layer k+1: F -> G[(k+1)&1] ---------------------------------
+    if (k + 1 < nz) {
+      dev::mbar_wait(bar, ph);
+      ph ^= 1u;
+      stage1(Gs + ((k + 1) & 1) * gsz);
+    }
+    __syncthreads();
+    // F is consumed: fetch layer k+2 behind the next phase's stages 3 and 2
+    if (tid == 0 && k + 2 < nz) {
+      dev::fence_proxy_async();
+      dev::mbar_expect_tx(bar, fbytes);
+      dev::tma_load_4d(Fs, &fmap, bar, xb0, xb1, (int)((int64_t)e_lo * Q + k + 2 - a.zpl), 0);
     }
   }
-  // trailing rows K2 + a (age a after the last element)
-  if (e_hi == a.K2 && e_lo < e_hi && tid < NPAIR) {
-    const double* ps = PS + tid;
+  // trailing rows K2 + ag (age ag after the last element)
+  if (e_hi == a.K2 && e_lo < e_hi && warp < NPW) {
+    uint32_t rr[32];
+    tmem_ld32(taddr, rr);
+    tmem_wait_ld();
 #pragma unroll
     for (int ag = 0; ag < P - 1; ++ag) {
       double row[W];
 #pragma unroll
-      for (int k = 0; k < W; ++k) row[k] = k < PD::len(ag) ? ps[(PD::off(ag) + k) * NPAIR] : 0.0;
+      for (int kx = 0; kx < W; ++kx)
+        row[kx] = kx < PD::len(ag) ? u2d(rr[2 * (PD::off(ag) + kx)], rr[2 * (PD::off(ag) + kx) + 1]) : 0.0;
       IGS_SYM_STORE(a.K2 + ag, row);
     }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(*tmem_holder));
   }
 }
 
