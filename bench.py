@@ -14,7 +14,10 @@ time, max over ranks); e2e = the same through the public API with host
 (pinned) x/y and the H2D/D2H copies inside the timed region; roofline of
 the dominant kernel (apply3d) against the measured HBM copy bandwidth;
 cpu_baseline = the CPU oracle (oracle/igs_oracle.py, a numpy restatement
-of the reference algorithm) on a bounded z-slab sample.
+of the reference algorithm) on a bounded z-slab sample.  The same line
+carries `c5` (the largest single-GPU config, 50 applies, with its own
+roofline / e2e / cpu_baseline) and `assembly` (C3 and C2, each checked
+against the oracle's values in the run).
 """
 
 import argparse
@@ -31,8 +34,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 WORKLOADS = {
-    "C4": dict(d=3, p=6, K=128, kind=2, desc="d3 p6 128^3 stiffness apply"),
-    "C5": dict(d=3, p=8, K=128, kind=3, desc="d3 p8 128^3 mass+stiffness apply"),
+    "C4": dict(d=3, p=6, K=128, kind=2, applies=100, desc="d3 p6 128^3 stiffness apply"),
+    "C5": dict(d=3, p=8, K=128, kind=3, applies=50, desc="d3 p8 128^3 mass+stiffness apply"),
 }
 
 
@@ -43,6 +46,52 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def fp64_peak():
+    """P64 (TFLOP/s): the DMMA rate tools/fp64_peak.py measured on this pool's
+    B200 with its clock record (profiles/fp64_peak.json), sustained figure."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["dmma_tflops_sustained"]), "profiles/fp64_peak.json (sustained DMMA, SM clock " \
+            f"{d['clocks_sustained']['sm_mhz']:.0f} MHz, reasons {d['clocks_sustained']['reasons']})"
+    except Exception:
+        return 37.15, "fallback (round-1 burst microbenchmark)"
+
+
+def ncu_profile(name):
+    """ncu-measured per-launch facts committed under profiles/ (F_exec, DRAM traffic)."""
+    try:
+        with open(os.path.join(REPO, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def config_for(name, world):
+    """The workload's config dict — identical in both arms (no torch needed)."""
+    w = WORKLOADS[name]
+    d, p, K = w["d"], w["p"], w["K"]
+    nplanes = {1: 1, 2: d * (d + 1) // 2, 3: 1 + d * (d + 1) // 2}[w["kind"]]
+    pts = (p * K) ** d
+    return {"workload": name, "desc": w["desc"], "dofs": (K + p - 1) ** d, "points": pts, "planes": nplanes,
+            "applies_per_step": 1, "baseline_applies": w["applies"],
+            "partition": f"slowest-axis slabs x{world}",
+            "l2": f"inputs > L2 ({8 * nplanes * pts / 1e9:.1f} GB of coefficient planes per step)"}
 
 
 class ClockSampler:
@@ -111,7 +160,8 @@ def cpu_baseline(w, min_seconds=10.0, seed=0):
     the numpy restatement of the reference algorithm) on a bounded sample:
     one element layer of the last direction per task, all host cores, passes
     repeated until `min_seconds` of work.  Coefficient values do not change
-    the work, so one layer of seeded planes is reused for every layer."""
+    the work, so one layer of seeded planes (1 + 0.05·U) is reused for every
+    layer; the rate is extrapolated from the layers done to whole applies."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import igs_oracle as O
@@ -142,19 +192,32 @@ def cpu_baseline(w, min_seconds=10.0, seed=0):
                 break
     t = time.perf_counter() - t0
     frac = done / K
-    return {"value": n * frac / t, "unit": "DoF/s", "cores": cores, "kind": "port",
-            "sample": f"{done} element layers ({frac:.2f} applies' worth) of {w['desc']}, "
-                      f"numpy oracle apply_slab on {cores} threads, {t:.1f} s"}
+    return {"value": n * frac / t, "unit": "DoF/s", "cores": cores, "kind": "port", "host": host_info(),
+            "sample": f"{done} element layers ({frac:.2f} applies' worth, extrapolated to whole applies) of "
+                      f"{w['desc']}, numpy oracle apply_slab on {cores} threads, one seeded layer of planes "
+                      f"(1 + 0.05 U) reused for every layer, {t:.1f} s"}
+
+
+def _sym_exec_model(p, K, e_cnt):
+    """Executed DMMA / fp64 flops of asm3_sym<4,4,4> from its schedule (used
+    only when the ncu-counted profiles/C3_fexec.json is absent): per (4x4-row
+    tile, z point) stage 1 = 4 y-tiles x 2 n-tiles x 5 k-steps x 10 blocks,
+    stage 2 = 4 m-tiles x 2 n-tiles x 4 k-steps x 9 groups DMMA (512 flop);
+    stage 3 = 448 pairs x (4P + 2P^2 FMA)."""
+    tiles = (-(-(K + p - 1) // 4)) ** 2
+    dmma = (400 + 288) * tiles * e_cnt * p
+    return 512.0 * dmma + 2.0 * 448 * (4 * p + 2 * p * p) * tiles * e_cnt * p
 
 
 def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
     """C3 assembly (d=3, p=4, 64^3, mass+stiffness) measured in the same run:
     warm assembly (pattern cached, as the reference caches it), CUDA events,
-    nnz/s; roofline against the measured fp64 DMMA peak; CPU baseline = the
-    oracle's Alg. 1 restatement on a reduced mesh (same p).  With N ranks the
+    nnz/s; roofline against the measured fp64 DMMA peak with F_exec counted
+    by ncu (profiles/C3_fexec.json); CPU baseline = the oracle's Alg. 1
+    restatement on the same full-size problem (one core).  With N ranks the
     rows are split by DoF layers of z (sharded.SlabAssembly): each rank
-    generates the coefficients of its slab plus a (p-1)-element halo and
-    writes its CSR slice, no collective; time = max over ranks."""
+    generates the coefficients of its slab plus the kernel's halo and writes
+    its CSR slice, no collective; time = max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -176,75 +239,59 @@ def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        run()
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     if world > 1:
         tt = torch.tensor([ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    # the dominant kernel (asm3_stage12) alone, same CUDA-event timing
-    # (IGS_FLAG_KERNEL_ONLY: values untouched)
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kone = (lambda: sumfac.assemble(prob, flags=4)) if world == 1 else None
-    k_ms = None
-    if kone is not None:
-        kone()
-        torch.cuda.synchronize()
-        k0.record()
-        for _ in range(reps):
-            kone()
-        k1.record()
-        torch.cuda.synchronize()
-        k_ms = k0.elapsed_time(k1) / reps
     nnz = prob.pattern().nnz
     npts = quad.num_points
     b_alg = 8 * field.n_planes * npts + 8 * nnz             # planes read + values written (whole job)
-    # achieved = max(B_alg/(t·BW), F_exec/(t·P64)), F_exec the
-    # fp64 flops the kernels execute.  Counted from the fused kernels' fixed
-    # schedule (cross-checked with ncu's DMMA-pipe utilisation):
-    #   asm3_stage12, per (4x4-row tile, z point): stage 1 = 4 y-tiles x 4
-    #   slot tiles x 10 blocks x 4 k-steps = 640 DMMA, stage 2 = 4 x 4 x 9
-    #   groups x 4 = 576 DMMA (512 flop each), over 17^2 tiles;
-    #   asm_sweep, per (slot pair, z point): the separable last-direction
-    #   contraction, 2P (mul + FMA) for u_0/u_1 and 2P^2 FMA into the ring
-    #   = 6P + 4P^2 flops; slot pairs padded to blocks of 128.
-    e_cnt = e_hi - e_lo
-    n_tiles = (-(-67 // 4)) ** 2
-    stage12 = 512 * (640 + 576) * n_tiles * (e_cnt * p)
-    slot_pairs = -(-(67 * 7) ** 2 // 128) * 128
-    sweep = (6 * p + 4 * p * p) * slot_pairs * (e_cnt * p)
-    f_exec = float(stage12 + sweep)
-    if world > 1:
-        tt = torch.tensor([f_exec], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt)
-        f_exec = float(tt.item())
-    # per-kernel composition: stage12 at the DMMA peak + the sweep's compulsory
-    # traffic (H read once, values written once) at the copy bandwidth
-    sweep_bytes = 8 * slot_pairs * (e_cnt * p) * 4 + 8 * nnz
+    p64, p64_src = fp64_peak()
+    p64 *= 1e12
+    prof = ncu_profile("C3_fexec.json")
+    if prof is not None and world == 1:
+        f_exec, f_src = float(prof["exec_flops"]), "ncu counters (profiles/C3_fexec.json)"
+        traffic = float(prof["dram_bytes"])
+    else:
+        f_exec, f_src = _sym_exec_model(p, K, e_hi - e_lo) * (world if world > 1 else 1), "kernel schedule"
+        traffic = None
     f_merged = 2 * 10_390_000_000        # merged-block MACs (the algorithm's own count)
     f_ref = 2 * 16_030_801_920           # the reference FlopCounter's block updates
-    p64 = 37.15e12 * world               # measured DMMA peak per GPU (profiles/r01_fp64_peak.txt)
     peak_bw, _ = measured_peak()
     t = ms / 1e3
+    fused = sumfac.fused_path(prob)
     out = {"workload": "C3", "desc": "d3 p4 64^3 mass+stiffness assembly (warm, pattern cached)",
-           "value": nnz / t, "unit": "nnz/s", "ms": ms, "nnz": nnz, "fused": sumfac.fused_path(prob),
-           "partition": f"z DoF-layer row blocks x{world} (slab + (p-1)-element halo, no collective)",
+           "value": nnz / t, "unit": "nnz/s", "ms": ms, "nnz": nnz, "fused": fused,
+           "kernel": "asm3_sym<4,4,4> (one pass: stages 1-3 on chip, symmetric half + mirrored writes)",
+           "gpu_launches_per_assembly": 2,
+           "partition": f"z DoF-layer row blocks x{world} (slab + halo, no collective)",
+           "clocks": clk.summary(),
            "roofline": {"bound": "fp64", "achieved": f_exec / t / 1e12, "peak": p64 / 1e12, "unit": "TFLOP/s",
-                        "frac": max(f_exec / t / p64, b_alg / t / (peak_bw * 1e9 * world)),
-                        "frac_rule": "SURVEY 8d: max(B_alg/(t BW), F_exec/(t P64)) over the whole assembly",
-                        "exec_flops": f_exec, "alg_flops_merged": f_merged, "ref_flops": f_ref,
-                        "frac_merged_alg": f_merged / t / p64, "frac_ref_equivalent": f_ref / t / p64,
-                        "hbm_gbs": b_alg / t / 1e9, "alg_bytes": b_alg,
-                        "frac_kernel_composed": (stage12 / (37.15e12) + sweep_bytes / (peak_bw * 1e9)) / world / t}}
-    if k_ms is not None:
-        out["roofline"]["dominant_kernel"] = {
-            "kernel": "asm3_stage12", "kernel_ms": k_ms, "exec_flops": float(stage12),
-            "achieved": stage12 / (k_ms / 1e3) / 1e12, "peak": 37.15, "unit": "TFLOP/s",
-            "frac": stage12 / (k_ms / 1e3) / 37.15e12}
+                        "peak_source": p64_src,
+                        "frac": max(f_exec / t / (p64 * world), b_alg / t / (peak_bw * 1e9 * world)),
+                        "frac_rule": "SURVEY 8d: max(B_alg/(t BW), F_exec/(t P64)); the one-pass kernel is "
+                                     "the whole assembly (plus a 1-thread row-offset launch)",
+                        "exec_flops": f_exec, "exec_flops_source": f_src, "alg_flops_merged": f_merged,
+                        "ref_flops": f_ref, "frac_merged_alg": f_merged / t / (p64 * world),
+                        "frac_ref_equivalent": f_ref / t / (p64 * world),
+                        "hbm_gbs": b_alg / t / 1e9, "alg_bytes": b_alg, "traffic": traffic}}
+    # the two-kernel fused path (H through HBM) on the same problem, for comparison
+    if world == 1:
+        sumfac.assemble(prob, flags=8)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            sumfac.assemble(prob, flags=8)
+        e1.record()
+        torch.cuda.synchronize()
+        out["two_pass_ms"] = e0.elapsed_time(e1) / reps
     # cold assembly (fresh problem: tabulation + pattern + values) and the CSR
     # hand-off to the host (f2), reported separately as SURVEY §8(d) asks
     if world == 1:
@@ -280,27 +327,40 @@ def assembly_section(reps=5, cpu=True, seed=0, rank=0, world=1):
         torch.cuda.synchronize()
         h2d_ms = e0.elapsed_time(e1)
         out["planes_h2d"] = {"ms": h2d_ms, "bytes": hpl.numel() * 8, "gbs": hpl.numel() * 8 / h2d_ms / 1e6}
+        out["e2e"] = {"value": nnz / ((ms + h2d_ms + d2h_ms) / 1e3), "unit": "nnz/s",
+                      "h2d_bytes_per_step": hpl.numel() * 8, "d2h_bytes_per_step": nbytes,
+                      "note": "warm assembly + planes upload + CSR download, each timed alone and summed"}
         del hpl, dpl
     if cpu and rank == 0 and world == 1:
         from oracle import igs_oracle as O
 
-        K = 24
         sp = [O.uniform_space(4, K) for _ in range(3)]
-        planes = O.synthetic_planes(3, [4 * K] * 3, 0, 4 * K, 3, seed)
+        hplanes = planes.cpu().numpy()
         ths = O.first_order_set(3)
         t0 = time.perf_counter()
-        vals = O.assemble_sumfac(sp, sp, ths, ths, planes, O.plane_map(3, 3))
-        t = time.perf_counter() - t0
-        out["cpu_baseline"] = {"value": vals.size / t, "unit": "nnz/s", "cores": 1, "kind": "port",
+        vals = O.assemble_sumfac(sp, sp, ths, ths, hplanes, O.plane_map(3, 3))
+        tc = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": vals.size / tc, "unit": "nnz/s", "cores": 1, "kind": "port",
+                               "host": host_info(),
                                "sample": f"oracle Alg. 1 restatement (scipy CSR x dense per direction, as the "
-                                         f"reference), p=4, {K}^3 elements, {vals.size} nnz, {t:.2f} s"}
+                                         f"reference), the full C3 problem on the same planes: {vals.size} nnz, "
+                                         f"{tc:.2f} s (values only, pattern excluded as in the warm GPU number)"}
+        err = float(np.linalg.norm(A_vals_check(prob) - vals) / np.linalg.norm(vals))
+        out["parity_vs_cpu"] = {"rel_frobenius": err, "tol": 1e-12}
+        assert err <= 1e-12, f"C3 GPU vs oracle {err:.3e}"
     return out
+
+
+def A_vals_check(prob):
+    from paper_1809_05471_b200 import sumfac
+
+    return sumfac.assemble(prob).values_np()
 
 
 def assembly_c2_section(reps=10, cpu=True, seed=0):
     """C2 (BASELINE configs[1]: d=2, p=5, 256², stiffness) assembly, warm,
     CUDA events; the CPU baseline is the oracle's Alg. 1 restatement on the
-    same full-size problem (one core)."""
+    same full-size problem (one core), whose values are also checked."""
     import torch
 
     from paper_1809_05471_b200 import sumfac, workloads
@@ -320,30 +380,43 @@ def assembly_c2_section(reps=10, cpu=True, seed=0):
     nnz = A.nnz
     b_alg = 8 * prob.coeff.n_planes * prob.quad.num_points + 8 * nnz
     f_ref = 2 * 460_800_000                   # the reference FlopCounter
+    p64, p64_src = fp64_peak()
     peak_bw, _ = measured_peak()
+    prof = ncu_profile("C2_fexec.json")
     out = {"workload": "C2", "desc": "d2 p5 256^2 stiffness assembly (warm, pattern cached)",
            "value": nnz / t, "unit": "nnz/s", "ms": ms, "nnz": nnz, "fused": sumfac.fused_path(prob),
-           "roofline": {"bound": "latency (kernel-launch and per-CTA latency at this size)",
-                        "frac_ref_equivalent": f_ref / t / 37.15e12, "hbm_frac": b_alg / t / (peak_bw * 1e9),
-                        "alg_bytes": b_alg, "ref_flops": f_ref}}
+           "roofline": {"bound": "fp64", "frac_ref_equivalent": f_ref / t / (p64 * 1e12),
+                        "hbm_frac": b_alg / t / (peak_bw * 1e9), "alg_bytes": b_alg, "ref_flops": f_ref,
+                        "peak": p64, "unit": "TFLOP/s", "peak_source": p64_src}}
+    if prof is not None:
+        out["roofline"]["exec_flops"] = float(prof["exec_flops"])
+        out["roofline"]["achieved"] = float(prof["exec_flops"]) / t / 1e12
+        out["roofline"]["frac"] = max(float(prof["exec_flops"]) / t / (p64 * 1e12), b_alg / t / (peak_bw * 1e9))
+        out["roofline"]["traffic"] = float(prof["dram_bytes"])
     if cpu:
         from oracle import igs_oracle as O
 
         sp = [O.uniform_space(p, K) for _ in range(2)]
-        planes = O.synthetic_planes(2, [p * K] * 2, 0, p * K, workloads.STIFF, seed)
+        planes = prob.coeff.planes.cpu().numpy()
         ths = O.first_order_set(2)
         t0 = time.perf_counter()
         vals = O.assemble_sumfac(sp, sp, ths, ths, planes, O.plane_map(2, workloads.STIFF))
         tc = time.perf_counter() - t0
+        err = float(np.linalg.norm(A.values_np() - vals) / np.linalg.norm(vals))
+        assert err <= 1e-12, f"C2 GPU vs oracle {err:.3e}"
+        out["parity_vs_cpu"] = {"rel_frobenius": err, "tol": 1e-12}
         out["cpu_baseline"] = {"value": vals.size / tc, "unit": "nnz/s", "cores": 1, "kind": "port",
-                               "sample": f"oracle Alg. 1 restatement, full C2 ({vals.size} nnz), {tc:.2f} s"}
+                               "host": host_info(),
+                               "sample": f"oracle Alg. 1 restatement, full C2 ({vals.size} nnz) on the same planes, "
+                                         f"{tc:.2f} s"}
     return out
 
 
-def run_reference(args, w):
+def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    w = WORKLOADS[args.workload]
     steps = []
     cb = None
     for i in range(args.warmup + args.steps):
@@ -353,38 +426,26 @@ def run_reference(args, w):
     value = float(np.median(steps))
     line = {"metric": "matrix-free fp64 apply throughput", "value": value, "unit": "DoF/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "desc": w["desc"]},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based coefficients, see DESIGN.md)",
+            "config": config_for(args.workload, world),
             "cpu_baseline": {**cb, "value": value},
             "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-assembly", action="store_true")
-    args = ap.parse_args()
-    w = WORKLOADS[args.workload]
-    if args.impl == "reference":
-        run_reference(args, w)
-        return
-
+def measure_apply(name, args, rank, world, local, steps, with_cpu):
+    """One apply workload (C4 / C5): device-timed steps, the dominant kernel
+    alone (roofline), e2e through the public API with host buffers, clocks,
+    and (rank 0, N=1) the CPU baseline.  Returns the result dict (rank 0)."""
     import torch
     import torch.distributed as dist
 
     from paper_1809_05471_b200 import matfree, workloads
     from paper_1809_05471_b200.sharded import ShardedApply, SlabPartition
+    from paper_1809_05471_b200.sumfac import AssemblyProblem
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = WORKLOADS[name]
     d, p, K, kind = w["d"], w["p"], w["K"], w["kind"]
     part = SlabPartition(K, p, world)
     lo, hi = part.elements(rank)
@@ -393,8 +454,6 @@ def main():
     planes = workloads.synthetic_planes(d, list(quad.shape), kind, seed=0, z_range=(lo * p, hi * p))
     slab = None if world == 1 else (lo, hi)
     field = workloads.field_from_planes(d, kind, planes, quad.shape, slab=slab)
-    from paper_1809_05471_b200.sumfac import AssemblyProblem
-
     prob = AssemblyProblem(bases, bases, quad, field)
     op = matfree.MatrixFreeOperator(prob)
     N = int(np.prod([b.num_basis for b in bases]))
@@ -407,6 +466,7 @@ def main():
     if world == 1:
         def step(x, y):
             op.apply_device(x, y)
+        launches = 2
     else:
         split = None
         if rank < world - 1 and hi - lo > p - 1:
@@ -420,6 +480,7 @@ def main():
             split = (lambda xv, yv: op_int.apply_device(xv, yv),
                      lambda xv, yv: op_bnd.apply_device(xv, yv, accumulate=True))
         sharded = ShardedApply(part, rank, layer_n, lambda xl, yl: op.apply_device(xl, yl), "cuda", split=split)
+        launches = 6
 
         def step(x, y):
             sharded.apply(x, y)
@@ -433,12 +494,12 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    # --- device-timed region: K applies, inputs (21.7+ GB) far larger than L2
+    # --- device-timed region: `steps` applies, inputs (21.7+ GB) far larger than L2
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(local) as clk:
         e0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             step(x_own, y_own)
         e1.record()
         barrier()
@@ -447,8 +508,7 @@ def main():
         tt = torch.tensor([t_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
-    ms_per_step = t_ms / args.steps
-    value = N * args.steps / (t_ms / 1e3)
+    value = N * steps / (t_ms / 1e3)
 
     # --- dominant kernel alone (apply3d, no reduce): roofline
     f = prob.coeff
@@ -457,7 +517,7 @@ def main():
     b_alg = 8 * f.n_planes * npts_local + 16 * n_local
     x_local = torch.randn(n_local, dtype=torch.float64, device="cuda", generator=gen)
     y_local = torch.empty(n_local, dtype=torch.float64, device="cuda")
-    kreps = max(5, args.steps // 2)
+    kreps = max(5, steps // 4)
     torch.cuda.synchronize()
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k0.record()
@@ -469,12 +529,9 @@ def main():
     peak, peak_kind = measured_peak()
     achieved = b_alg / (k_ms / 1e3) / 1e9
     traffic = None
-    prof = os.path.join(REPO, "profiles", f"{args.workload}_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    prof = ncu_profile(f"{name}_traffic.json")
+    if prof is not None:
+        traffic = prof.get("dram_bytes_per_launch")
 
     # --- end to end through the public API: pinned host x -> device -> apply
     # -> host y every step, transfers overlapped with the neighbouring steps'
@@ -486,7 +543,7 @@ def main():
     pipe.run([x_host] * 2, y_hosts)
     barrier()
     e0.record()
-    pipe.run([x_host] * args.steps, [y_hosts[i & 1] for i in range(args.steps)])
+    pipe.run([x_host] * steps, [y_hosts[i & 1] for i in range(steps)])
     e1.record()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
@@ -494,12 +551,54 @@ def main():
         tt = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_value = N * args.steps / (e2e_ms / 1e3)
+    e2e_value = N * steps / (e2e_ms / 1e3)
     fused_flag = op.fused
+    del planes, field, prob, op
+    if world == 1:
+        step = None
+    torch.cuda.empty_cache()
+    cb = cpu_baseline(w) if (with_cpu and rank == 0 and world == 1) else None
+    return {"value": value, "unit": "DoF/s", "steps": steps, "ms_per_step": t_ms / steps,
+            "config": config_for(name, world), "fused": fused_flag,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "apply3d_kernel", "kernel_ms": k_ms, "alg_bytes_per_launch": b_alg},
+            "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * n_own,
+                    "d2h_bytes_per_step": 8 * n_own},
+            "gpu_launches": steps * launches, "clocks": clk.summary(), "cpu_baseline": cb}
 
-    cb = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline(w)
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100, help="applies per timed region (BASELINE C4: 100)")
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-assembly", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 section (the C4 run measures C5 too)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res = measure_apply(args.workload, args, rank, world, local, args.steps, not args.no_cpu_baseline)
+    c5 = None
+    if args.workload == "C4" and not args.no_c5:
+        # the largest single-GPU configuration (60 GB of planes), BASELINE's 50 applies
+        try:
+            c5 = measure_apply("C5", args, rank, world, local, WORKLOADS["C5"]["applies"],
+                               not args.no_cpu_baseline)
+        except Exception as exc:  # the headline line must still print
+            c5 = {"error": repr(exc)}
     asm = None
     if not args.no_assembly:
         try:
@@ -510,25 +609,15 @@ def main():
             asm = {"error": repr(exc)}
     if rank == 0:
         line = {
-            "metric": "matrix-free fp64 apply throughput", "value": value, "unit": "DoF/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "metric": "matrix-free fp64 apply throughput", "value": res["value"], "unit": "DoF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based coefficients, see DESIGN.md)",
-            "config": {"workload": args.workload, "desc": w["desc"], "dofs": N,
-                       "points": quad.num_points, "planes": f.n_planes,
-                       "partition": f"slowest-axis slabs x{world}", "l2": "inputs > L2 (21.7+ GB per step)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "apply3d_kernel", "kernel_ms": k_ms, "alg_bytes_per_launch": b_alg},
-            "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * n_own,
-                    "d2h_bytes_per_step": 8 * n_own},
+            "config": res["config"], "roofline": res["roofline"], "e2e": res["e2e"],
             # per step: apply3d + reduce; rank 0 of a slab run: x copy, interior
             # and boundary applies (2 + 2), y copy (K5 kernels) — NCCL's own excluded
-            "gpu_launches": args.steps * (2 if world == 1 else 6),
-            "clocks": clk.summary(),
-            "cpu_baseline": cb,
-            "fused": fused_flag,
-            "assembly": asm,
+            "gpu_launches": res["gpu_launches"], "clocks": res["clocks"], "cpu_baseline": res["cpu_baseline"],
+            "fused": res["fused"], "c5": c5, "assembly": asm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

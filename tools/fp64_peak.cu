@@ -37,7 +37,22 @@ __global__ void copy_kernel(const double2* __restrict__ a, double2* __restrict__
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
-int main() {
+int main(int argc, char** argv) {
+  // "sustained": DMMA kernels back to back for ~4 s, average rate
+  if (argc > 1 && argv[1][0] == 's') {
+    cudaDeviceProp prop; cudaGetDeviceProperties(&prop, 0);
+    double* out; cudaMalloc(&out, 1 << 24);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    int blocks = prop.multiProcessorCount * 4, threads = 256, iters = 2000, reps = 480;
+    dmma_kernel<<<blocks, threads>>>(out, 10);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) dmma_kernel<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 2.0 * 8 * 8 * 4 * (blocks * threads / 32) * (double)iters * 16 * 4 * reps;
+    printf("{\"dmma_tflops_sustained\": %.2f, \"ms\": %.1f}\n", flops / ms / 1e9, ms);
+    return 0;
+  }
   cudaDeviceProp prop; cudaGetDeviceProperties(&prop, 0);
   printf("{\"name\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"smem_optin\": %zu, \"clock_khz\": %d, \"mem_clock_khz\": %d, \"bus_bits\": %d, \"regs_per_sm\": %d}\n",
          prop.name, prop.multiProcessorCount, prop.l2CacheSize, prop.sharedMemPerBlockOptin, prop.clockRate,
