@@ -94,7 +94,6 @@ struct SymCfg {
                sizeof(double) + 32;
   }
   static_assert(XR1 <= 256 && XB0 <= 256, "TMA box");
-  static_assert(NPAIR <= NT, "one pair per thread");
 };
 
 struct SymArgs {
@@ -295,6 +294,7 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int KS0 = C::KS0, W0R = C::W0R, KS1 = C::KS1, W1P = C::W1P, PP = C::PP, FZ = C::FZ;
   constexpr int NT = C::NT, NW = C::NW, NPAIR = C::NPAIR, NPW = (NPAIR + 31) / 32;
   static_assert(2 * PD::N <= 32, "pending rows fit a 32-column TMEM slice");
+  static_assert(NPAIR <= NT, "one pair per thread");
   extern __shared__ __align__(128) double sm[];
   const int ng = a.plan.ng;
   const size_t fb = C::fbuf(a.nplanes);

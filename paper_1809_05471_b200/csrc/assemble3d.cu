@@ -1274,7 +1274,6 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
     igs_status r = IGS_ECAPACITY;
     switch (P) {
       case 2: r = launch3_sym<2>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
-      case 3: r = launch3_sym<3>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
       case 4: r = launch3_sym<4>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
       default: break;
     }

@@ -1,7 +1,7 @@
 """The one-pass symmetric 3D assembly (csrc/asm3_sym.cuh) against the oracle.
 
 For symmetric problems (trial == test, first-order sets, F_{η,θ} = F_{θ,η})
-the fused 3D assembly forms only the x-pairs with n0 >= m0 and writes each
+the fused 3D assembly (asm3_sym) forms only the x-pairs with n0 >= m0 and writes each
 value to its row and, mirrored, to the transposed entry.  Checked here:
   * pattern identical and values within 1e-12 (relative Frobenius) of the
     oracle's independent Kronecker assembly (sumfac.py:480-509 form) and of
@@ -33,10 +33,11 @@ def _problem(p, K, kind, seed):
     from paper_1809_05471_b200.bspline import UnivariateBasis, uniform_open_knots
     from paper_1809_05471_b200.quadrature import TensorQuadrature, per_element_rule
 
+    d = len(K)
     bases = [UnivariateBasis(uniform_open_knots(p, k)) for k in K]
     quad = TensorQuadrature([per_element_rule(b.breakpoints, p) for b in bases])
-    planes = workloads.synthetic_planes(3, list(quad.shape), kind, seed=seed)
-    return sumfac.AssemblyProblem(bases, bases, quad, workloads.field_from_planes(3, kind, planes, quad.shape)), planes
+    planes = workloads.synthetic_planes(d, list(quad.shape), kind, seed=seed)
+    return sumfac.AssemblyProblem(bases, bases, quad, workloads.field_from_planes(d, kind, planes, quad.shape)), planes
 
 
 def _rel(a, b):
@@ -53,9 +54,10 @@ def test_sym_assembly_vs_oracle_and_two_pass(cuda, p, K, kind):
     assert sumfac.fused_path(prob) == 1
     A = sumfac.assemble(prob)
     B = sumfac.assemble(prob, flags=TWO_PASS)
+    d = len(K)
     sp = [O.uniform_space(p, k) for k in K]
-    ths = O.first_order_set(3)
-    Ar = O.assemble_kron(sp, sp, ths, ths, O.dense_field(planes.cpu().numpy(), O.plane_map(3, kind)))
+    ths = O.first_order_set(d)
+    Ar = O.assemble_kron(sp, sp, ths, ths, O.dense_field(planes.cpu().numpy(), O.plane_map(d, kind)))
     pairs = [O.pattern_1d(s.lo, s.hi, s.lo, s.hi, s.points) for s in sp]
     indptr, indices = O.tensor_csr(pairs, [s.num_basis for s in sp], [s.num_basis for s in sp])
     np.testing.assert_array_equal(prob.pattern().indptr, indptr)
@@ -78,7 +80,7 @@ def test_sym_assembly_row_ranges_bit_identical(cuda, p, K, kind):
     full = sumfac.assemble(prob).values_np()
     pat = prob.pattern()
     nrows = pat.shape[0]
-    layer = nrows // (K[2] + p - 1)
+    layer = nrows // (K[-1] + p - 1)
     for cuts in ([0, nrows // 3, (2 * nrows) // 3, nrows],             # partial layers
                  [0, 2 * layer, 5 * layer, nrows],                     # whole layers
                  [0, 1, nrows - 1, nrows]):                            # single rows
