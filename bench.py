@@ -442,7 +442,7 @@ def measure_apply(name, args, rank, world, local, steps, with_cpu):
     import torch.distributed as dist
 
     from paper_1809_05471_b200 import matfree, workloads
-    from paper_1809_05471_b200.sharded import ShardedApply, SlabPartition
+    from paper_1809_05471_b200.sharded import NcclComm, NcclSlabApply, SlabPartition
     from paper_1809_05471_b200.sumfac import AssemblyProblem
 
     w = WORKLOADS[name]
@@ -468,19 +468,12 @@ def measure_apply(name, args, rank, world, local, steps, with_cpu):
             op.apply_device(x, y)
         launches = 2
     else:
-        split = None
-        if rank < world - 1 and hi - lo > p - 1:
-            # overlap: interior elements run while the ghost layers arrive
-            cut = hi - p + 1
-            npc = (cut - lo) * p * layer_pts
-            op_int = matfree.MatrixFreeOperator(AssemblyProblem(
-                bases, bases, quad, workloads.field_from_planes(d, kind, planes[:, :npc], quad.shape, slab=(lo, cut))))
-            op_bnd = matfree.MatrixFreeOperator(AssemblyProblem(
-                bases, bases, quad, workloads.field_from_planes(d, kind, planes[:, npc:], quad.shape, slab=(cut, hi))))
-            split = (lambda xv, yv: op_int.apply_device(xv, yv),
-                     lambda xv, yv: op_bnd.apply_device(xv, yv, accumulate=True))
-        sharded = ShardedApply(part, rank, layer_n, lambda xl, yl: op.apply_device(xl, yl), "cuda", split=split)
-        launches = 6
+        # the C-ABI data plane: igs_apply_sharded over an NCCL communicator of
+        # the library (ghost gather on a communication stream overlapped with
+        # the interior elements, boundary elements after it, ghost reduce)
+        comm = NcclComm(rank, world)
+        sharded = NcclSlabApply(op, part, rank, comm=comm, overlap=True)
+        launches = 8  # x copy, interior apply3d + reduce, memset, boundary apply3d + reduce, halo add, y copy
 
         def step(x, y):
             sharded.apply(x, y)
@@ -553,9 +546,12 @@ def measure_apply(name, args, rank, world, local, steps, with_cpu):
         e2e_ms = float(tt.item())
     e2e_value = N * steps / (e2e_ms / 1e3)
     fused_flag = op.fused
+    if world > 1:
+        comm.check()
+        dist.barrier()
+        comm.close()
     del planes, field, prob, op
-    if world == 1:
-        step = None
+    step = None
     torch.cuda.empty_cache()
     cb = cpu_baseline(w) if (with_cpu and rank == 0 and world == 1) else None
     return {"value": value, "unit": "DoF/s", "steps": steps, "ms_per_step": t_ms / steps,

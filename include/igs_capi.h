@@ -107,8 +107,10 @@ enum {
                                    values untouched; the one-pass symmetric assembly is a
                                    single kernel and runs whole) — the roofline's
                                    dominant kernel                                       */
-  IGS_FLAG_TWO_PASS = 8         /* assembly: the two-kernel fused path (intermediate H in
+  IGS_FLAG_TWO_PASS = 8,        /* assembly: the two-kernel fused path (intermediate H in
                                    HBM) even where the one-pass symmetric kernel applies */
+  IGS_FLAG_SPLIT_BOUNDARY = 16  /* igs_apply_sharded: interior / boundary launches even
+                                   without a next rank (exercises the overlap path)     */
 };
 
 /* ---- diagnostics ---------------------------------------------------- */
@@ -273,6 +275,35 @@ igs_status igs_geometry_planes(const igs_geometry_map* map, const igs_pullback_a
  * as kernels so they can be captured in CUDA graphs. dst[i] (+)= src[i]. */
 igs_status igs_layers_copy(const double* src, double* dst, int64_t count, int32_t add,
                            void* stream);
+
+/* ---- multi-GPU data plane ----------------------- */
+/* NCCL communicators for the slab partition.  NCCL is resolved at run time
+ * (libnccl.so.2 already loaded by the host process, else the system one);
+ * `comm` is an ncclComm_t passed as void*.  Failures return IGS_ENCCL with
+ * NCCL's message in igs_last_error(). */
+igs_status igs_nccl_unique_id(uint8_t* id /* host [128] */);
+igs_status igs_nccl_comm_init(const uint8_t* id /* host [128] */, int32_t nranks, int32_t rank,
+                              void** comm /* host out */);
+igs_status igs_nccl_comm_destroy(void* comm);
+/* Asynchronous communicator error (peer failure, transport error, timeout
+ * detected by NCCL) -> IGS_ENCCL; with abort_on_error the communicator is
+ * aborted so pending operations return. */
+igs_status igs_nccl_check(void* comm, int32_t abort_on_error);
+
+/* One rank's part of y = A x for the slab partition along the last
+ * direction (replaces the reference's single-process matvec, sumfac.py:112,
+ * for the SPEC apply): `prob` carries this rank's slab
+ * [slab_lo, slab_hi) (rank 0 owns element 0, the last rank the last one),
+ * `planes` that slab's coefficient points; x_own / y_own hold the rank's own
+ * DoF layers [slab_lo, slab_hi) (the last rank also the trailing order-1
+ * layers).  The (order-1)-layer halo moves by NCCL send/recv: ghost gather
+ * of x from rank+1, ghost reduce of y into rank+1.  With `comm_stream` (may
+ * be NULL) the gather overlaps the interior elements.  `comm` may be NULL
+ * for nranks = 1. */
+size_t igs_apply_sharded_workspace(const igs_problem* prob, int32_t rank, int32_t nranks, int32_t flags);
+igs_status igs_apply_sharded(const igs_problem* prob, const double* planes, const double* x_own, double* y_own,
+                             void* ws, size_t ws_bytes, void* comm, int32_t rank, int32_t nranks,
+                             int32_t flags, void* stream, void* comm_stream);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ MAX_ORDER = 16
 
 OP_ASSEMBLE, OP_APPLY, OP_EVAL_FIELD, OP_PATTERN = 1, 2, 3, 4
 FLAG_DEFAULT, FLAG_FORCE_GENERIC, FLAG_ACCUMULATE = 0, 1, 2
+FLAG_KERNEL_ONLY, FLAG_TWO_PASS, FLAG_SPLIT_BOUNDARY = 4, 8, 16
 
 IGS_OK, IGS_EARG, IGS_EDOMAIN, IGS_EDERIV, IGS_ECAPACITY, IGS_ECUDA, IGS_ENCCL, IGS_EWORKSPACE = range(8)
 
@@ -142,6 +143,17 @@ _SIGNATURES = [
     ("igs_geometry_pullback", ctypes.c_int,
      [ctypes.POINTER(IgsPullbackArgs), ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
       ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_size_t,
+      ctypes.c_void_p]),
+    ("igs_nccl_unique_id", ctypes.c_int, [ctypes.c_void_p]),
+    ("igs_nccl_comm_init", ctypes.c_int,
+     [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    ("igs_nccl_comm_destroy", ctypes.c_int, [ctypes.c_void_p]),
+    ("igs_nccl_check", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    ("igs_apply_sharded_workspace", ctypes.c_size_t,
+     [ctypes.POINTER(IgsProblem), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    ("igs_apply_sharded", ctypes.c_int,
+     [ctypes.POINTER(IgsProblem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+      ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
       ctypes.c_void_p]),
 ]
 

@@ -36,6 +36,7 @@ SOURCES = [
     "assemble3d.cu",
     "geometry.cu",
     "naive.cu",
+    "sharded.cu",
     "mmio.cpp",
 ]
 
@@ -88,7 +89,7 @@ def build(verbose=False, force=False):
     objs = [r[0] for r in results]
     changed = any(r[1] for r in results)
     if changed or not os.path.exists(LIB_PATH) or force:
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB_PATH, *objs, "-lcudart", "-lcuda", "-lgomp"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB_PATH, *objs, "-lcudart", "-lcuda", "-lgomp", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")

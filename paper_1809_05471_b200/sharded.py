@@ -106,17 +106,30 @@ class ShardedApply:
         self.y_local = torch.zeros(self.n_local, dtype=dtype, device=device)
         self.halo_in = torch.zeros((part.p - 1) * self.layer, dtype=dtype, device=device)
 
+    def _staged(self):
+        """Device tensors over a CPU-only backend (gloo): the halo is staged
+        through host buffers (the multi-process tests run the CUDA kernels of
+        every rank on one GPU this way)."""
+        if not self.x_local.is_cuda or not dist.is_initialized():
+            return False
+        return dist.get_backend(self.group) == "gloo"
+
     def _start(self, send, recv):
         ops = []
+        back = []
+        staged = bool(send or recv) and self._staged()
         for buf, peer in send:
-            ops.append(dist.P2POp(dist.isend, buf, peer, group=self.group))
+            ops.append(dist.P2POp(dist.isend, buf.cpu() if staged else buf, peer, group=self.group))
         for buf, peer in recv:
-            ops.append(dist.P2POp(dist.irecv, buf, peer, group=self.group))
-        return dist.batch_isend_irecv(ops) if ops else []
+            tgt = torch.empty(buf.shape, dtype=buf.dtype) if staged else buf
+            if staged:
+                back.append((tgt, buf))
+            ops.append(dist.P2POp(dist.irecv, tgt, peer, group=self.group))
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return _Pending(reqs, back)
 
     def _exchange(self, send, recv):
-        for req in self._start(send, recv):
-            req.wait()
+        self._start(send, recv).wait()
 
     def apply(self, x_own, y_own=None):
         """y_own = (A x) restricted to this rank's own DoF layers."""
@@ -132,11 +145,10 @@ class ShardedApply:
         p = self.part.p
         if self.split is not None and r < W - 1 and hi - lo > p - 1:
             # 2a. interior elements while the ghosts are in flight
-            reqs = self._start(send, recv)
+            pending = self._start(send, recv)
             interior, boundary = self.split
             interior(self.x_local[: self.n_own], self.y_local[: self.n_own])
-            for req in reqs:
-                req.wait()
+            pending.wait()
             # 2b. the last p-1 elements need the ghost layers
             b0 = (hi - lo - p + 1) * self.layer
             self.y_local[self.n_own:].zero_()
@@ -158,6 +170,98 @@ class ShardedApply:
         if y_own is not None:
             return layers_copy(y_own, out)
         return out
+
+
+class _Pending:
+    """Outstanding p2p requests; host-staged receives are copied to their
+    device buffers once complete."""
+
+    def __init__(self, reqs, back):
+        self.reqs = reqs
+        self.back = back
+
+    def wait(self):
+        for req in self.reqs:
+            req.wait()
+        for host, dev in self.back:
+            dev.copy_(host)
+
+
+class NcclComm:
+    """An NCCL communicator of the library (igs_nccl_comm_init) over the ranks
+    of a torch.distributed group: rank 0 draws the unique id, the group
+    broadcasts it.  world = 1 needs no torch.distributed."""
+
+    def __init__(self, rank, world, group=None):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = _lib
+        lib = _lib.load()
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _lib.check(lib.igs_nccl_unique_id(uid), "nccl_unique_id")
+        if world > 1:
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=0, group=group)
+            uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        self.handle = ctypes.c_void_p()
+        _lib.check(lib.igs_nccl_comm_init(uid, world, rank, ctypes.byref(self.handle)), "nccl_comm_init")
+        self.rank, self.world = int(rank), int(world)
+
+    def check(self, abort=True):
+        """Raise RuntimeError (IGS_ENCCL) on an asynchronous communicator error."""
+        self._lib.check(self._lib.load().igs_nccl_check(self.handle, int(bool(abort))), "nccl")
+
+    def close(self):
+        if self.handle:
+            self._lib.check(self._lib.load().igs_nccl_comm_destroy(self.handle), "nccl_comm_destroy")
+            self.handle = None
+
+
+class NcclSlabApply:
+    """One rank's slab apply through the C-ABI's NCCL data plane
+    (igs_apply_sharded): ghost gather overlapped with the interior elements
+    on a communication stream, the boundary elements after it, the ghost
+    reduce into the next rank.  `op` is the MatrixFreeOperator of the rank's
+    slab problem (coefficients of elements part.elements(rank))."""
+
+    def __init__(self, op, part, rank, comm=None, overlap=True, split_boundary=False):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = _lib
+        self.op = op
+        self.part = part
+        self.rank = int(rank)
+        self.comm = comm
+        if part.world > 1 and comm is None:
+            raise ValueError("more than one rank needs an NcclComm")
+        lib = _lib.load()
+        self.prob, self._keep = op.struct()
+        self.flags = (op.flags & _lib.FLAG_FORCE_GENERIC) | (_lib.FLAG_SPLIT_BOUNDARY if split_boundary else 0)
+        nbytes = lib.igs_apply_sharded_workspace(ctypes.byref(self.prob), self.rank, part.world, self.flags)
+        if nbytes == 0:
+            _lib.check(_lib.IGS_EARG, "apply_sharded_workspace")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.comm_stream = torch.cuda.Stream() if overlap else None
+
+    def apply(self, x_own, y_own):
+        import ctypes
+
+        lib = self._lib.load()
+        cs = ctypes.c_void_p(self.comm_stream.cuda_stream) if self.comm_stream is not None else None
+        handle = self.comm.handle if self.comm is not None else None
+        st = lib.igs_apply_sharded(ctypes.byref(self.prob), self._lib.ptr(self.op.problem.coeff_field().planes),
+                                   self._lib.ptr(x_own), self._lib.ptr(y_own), self._lib.ptr(self.ws),
+                                   self.ws.numel(), handle, self.rank, self.part.world, self.flags,
+                                   self._lib.stream_handle(), cs)
+        self._lib.check(st, "apply_sharded")
+        return y_own
 
 
 class SlabAssembly:
