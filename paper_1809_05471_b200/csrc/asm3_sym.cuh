@@ -25,6 +25,12 @@
 // (o1 in [-(P-1), P-1], rows padded to SR1 slots); tables are band tables
 // restricted to the k-steps each MMA tile can touch.
 
+// Measurement-only variants (tools/build_variant.sh; wrong values): 1 drops
+// stage 3, 2 stage 2, 3 stage 1 of the phase loop.  The library builds 0.
+#ifndef IGS_SYM_EXP
+#define IGS_SYM_EXP 0
+#endif
+
 template <int P, int T0, int T1>
 struct SymCfg {
   static constexpr int Q = P;
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int XB0 = C::XB0, XR1 = C::XR1, XRP1 = C::XRP1, NYT = C::NYT, SPG = C::SPG, HP = C::HP;
   constexpr int KS0 = C::KS0, W0R = C::W0R, KS1 = C::KS1, W1P = C::W1P, PP = C::PP, FZ = C::FZ;
   constexpr int NT = C::NT, NW = C::NW, NPAIR = C::NPAIR, NPW = (NPAIR + 31) / 32;
-  static_assert(2 * PD::N <= 32, "pending rows fit a 32-column TMEM slice");
+  static_assert(2 * PD::N <= 32 && 2 * P * P <= 32, "pending rows and E fit 32-column TMEM slices");
   static_assert(NPAIR <= NT, "one pair per thread");
   extern __shared__ __align__(128) double sm[];
   const int ng = a.plan.ng;
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(512, 1)
 
   // ---- prologue: TMEM, zeroed shared memory, tables, barrier, first layer ---
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
                      dev::smem_u32(tmem_holder)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -339,7 +345,9 @@ __global__ void __launch_bounds__(512, 1)
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t taddr = *tmem_holder + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(32 * (warp >> 2));
+  // per thread 64 TMEM columns of its lane: [0, 32) pending rows, [32, 64)
+  // the element matrix E[jm][jn] being accumulated (registers only in stage 3)
+  const uint32_t taddr = *tmem_holder + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
   dev::fence_proxy_async();
   __syncthreads();
   if (tid == 0 && nz > 0) {
@@ -354,6 +362,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = 0u;
     tmem_st32(taddr, z);
+    tmem_st32(taddr + 32, z);
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
   }
 
@@ -413,11 +422,6 @@ __global__ void __launch_bounds__(512, 1)
   const int lay_lo = (int)((a.row_lo + layer - 1) / layer), lay_hi = (int)(a.row_hi / layer);
   const int fw_lo = max(max(2 * (P - 1), r_lo + P - 1), lay_lo + P - 1);
   const int fw_hi = min(min(a.K2 - P + 1, r_hi - P + 1), lay_hi - P + 1);
-  double E[P][P];  // this element's contribution to rows e + jm, columns e + jn
-#pragma unroll
-  for (int i = 0; i < P; ++i)
-#pragma unroll
-    for (int j = 0; j < P; ++j) E[i][j] = 0.0;
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -483,6 +487,8 @@ __global__ void __launch_bounds__(512, 1)
       const int z = k - 1, es = e_lo + z / Q, qs = z % Q;
       const double* fq = FZs + ((es - e_lo) & 1) * FZ + qs * 4 * PP;
       const double* hcol = Hs + (z & 1) * C::HS + s1c * HP + s0;
+      uint32_t er[32];
+      tmem_ld32(taddr + 32, er);  // E of this element so far, in flight during the smem loads
       double hv[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) hv[v] = a.vmap[v] >= 0 ? hcol[a.vmap[v] * (C::NS1C * HP)] : 0.0;
@@ -500,6 +506,12 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
       // Σ_{θ,η} (w·B^θ_jn)(B^η_jm) H_{θ+2η}: θ first (u_η[jn]), then η
+      tmem_wait_ld();
+      double E[P][P];
+#pragma unroll
+      for (int jm = 0; jm < P; ++jm)
+#pragma unroll
+        for (int jn = 0; jn < P; ++jn) E[jm][jn] = u2d(er[2 * (jm * P + jn)], er[2 * (jm * P + jn) + 1]);
       double u0[P], u1[P];
 #pragma unroll
       for (int jn = 0; jn < P; ++jn) {
@@ -543,6 +555,14 @@ __global__ void __launch_bounds__(512, 1)
           for (int j = 0; j < P; ++j) E[i][j] = 0.0;
         IGS_SYM_STORE(es, row);
       }
+#pragma unroll
+      for (int jm = 0; jm < P; ++jm)
+#pragma unroll
+        for (int jn = 0; jn < P; ++jn) {
+          er[2 * (jm * P + jn)] = (uint32_t)__double2loint(E[jm][jn]);
+          er[2 * (jm * P + jn) + 1] = (uint32_t)__double2hiint(E[jm][jn]);
+        }
+      tmem_st32(taddr + 32, er);
     }
   };
 
@@ -551,7 +571,9 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
   for (int k = 0; k <= nz; ++k) {
     // ---- stage 3 of layer k-1 ------------------------------------------------
+#if IGS_SYM_EXP != 1
     stage3(k);
+#endif
     // next element's z factors: loaded at the first layer of an element (in
     // stage 3 terms), stored one phase later (the other buffer's last reader,
     // the previous element's stage 3, finished two barriers before)
@@ -570,7 +592,7 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
     // ---- stage 2 of layer k: G[k&1] -> H[k&1] ---------------------------------
-    if (k < nz) {
+    if (k < nz && IGS_SYM_EXP != 2) {
       const double* Gb = Gs + (k & 1) * gsz;
       double* Hb = Hs + (k & 1) * C::HS;
       for (int t = warp; t < nt2; t += NW) {
@@ -614,7 +636,9 @@ __global__ void __launch_bounds__(512, 1)
     if (k + 1 < nz) {
       dev::mbar_wait(bar, ph);
       ph ^= 1u;
+#if IGS_SYM_EXP != 3
       stage1(Gs + ((k + 1) & 1) * gsz);
+#endif
     }
     __syncthreads();
     // F is consumed: fetch layer k+2 behind the next phase's stages 3 and 2
@@ -642,7 +666,7 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(*tmem_holder));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(*tmem_holder));
   }
 }
 
