@@ -26,9 +26,16 @@
 // restricted to the k-steps each MMA tile can touch.
 
 // Measurement-only variants (tools/build_variant.sh; wrong values): 1 drops
-// stage 3, 2 stage 2, 3 stage 1 of the phase loop.  The library builds 0.
+// stage 3, 2 stage 2, 3 stage 1 of the phase loop, 4 the CSR stores of the
+// finished rows.  The library builds 0.
 #ifndef IGS_SYM_EXP
 #define IGS_SYM_EXP 0
+#endif
+// Where stage 3 runs in a phase (measurement variants): 0 first, 1 last,
+// 2 first on half the warps and last on the others (the library: each SMSP
+// then mixes stage-3 FMA work with the other warps' DMMA work).
+#ifndef IGS_SYM_S3_ORDER
+#define IGS_SYM_S3_ORDER 2
 #endif
 
 template <int P, int T0, int T1>
@@ -553,7 +560,9 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = 0; i < P; ++i)
 #pragma unroll
           for (int j = 0; j < P; ++j) E[i][j] = 0.0;
+#if IGS_SYM_EXP != 4
         IGS_SYM_STORE(es, row);
+#endif
       }
 #pragma unroll
       for (int jm = 0; jm < P; ++jm)
@@ -571,8 +580,10 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
   for (int k = 0; k <= nz; ++k) {
     // ---- stage 3 of layer k-1 ------------------------------------------------
-#if IGS_SYM_EXP != 1
+#if IGS_SYM_EXP != 1 && IGS_SYM_S3_ORDER == 0
     stage3(k);
+#elif IGS_SYM_S3_ORDER == 2
+    if (((warp >> 2) & 1) == 0) stage3(k);
 #endif
     // next element's z factors: loaded at the first layer of an element (in
     // stage 3 terms), stored one phase later (the other buffer's last reader,
@@ -640,6 +651,11 @@ __global__ void __launch_bounds__(512, 1)
       stage1(Gs + ((k + 1) & 1) * gsz);
 #endif
     }
+#if IGS_SYM_S3_ORDER == 1
+    stage3(k);
+#elif IGS_SYM_S3_ORDER == 2
+    if (((warp >> 2) & 1) == 1) stage3(k);
+#endif
     __syncthreads();
     // F is consumed: fetch layer k+2 behind the next phase's stages 3 and 2
     if (tid == 0 && k + 2 < nz) {
