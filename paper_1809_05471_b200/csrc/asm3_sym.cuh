@@ -126,8 +126,11 @@ struct SymArgs {
   int hsplit;            // stage-2 groups [0, hsplit) | [hsplit, ng) (whole stage-2 groups)
   int vmap[4];           // stage-2 group holding z variant v = θ + 2η (-1: none)
   // compact plan for the kernel's runtime loops
-  int b_plane[kMaxBlocks], b_v0[kMaxBlocks], b_g[kMaxBlocks];  // per block (group order)
+  int b_plane[kMaxBlocks], b_v0[kMaxBlocks], b_g[kMaxBlocks];  // stage-1 blocks (group order)
+  int nb1, half_b1;       // stage-1 blocks, split into two halves at a group boundary
   int g_v1[kMaxBlocks], g_h[kMaxBlocks];                       // per stage-1 group
+  int g_src[kMaxBlocks];  // G buffer stage 2 reads for group g (groups with identical
+                          // (plane, x variant) block sets share one stage-1 result)
   unsigned b_end, g_end;  // bit b: last block of its group; bit g: last group of its stage-2 group
 };
 
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(512, 1)
   auto stage1 = [&](double* Gb) {
     for (int t = warp; t < nt1; t += NW) {
       const int yt = t % NYT, st = (t / NYT) % NST0, half = t / (NYT * NST0);
-      const int b_lo = half ? a.plan.half_b : 0, b_hi = half ? a.plan.nb : a.plan.half_b;
+      const int b_lo = half ? a.half_b1 : 0, b_hi = half ? a.nb1 : a.half_b1;
       int klo = 0;
 #pragma unroll
       for (int i = 0; i < NST0; ++i)
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
         for (int g = g_lo; g < g_hi; ++g) {
           const double* Wg = Wk + a.g_v1[g] * (NMT1 * 8 * W1P);
-          const double* Gg = Gk + g * (XRP1 * SPG);
+          const double* Gg = Gk + a.g_src[g] * (XRP1 * SPG);
           double wv[KS1], gv[KS1];
 #pragma unroll
           for (int kk = 0; kk < KS1; ++kk) {
@@ -770,11 +773,50 @@ igs_status launch3_sym(const igs_problem* p, const AsmShape& s, TensorPat pat, i
   }
   for (int v = 0; v < 4; ++v) a.vmap[v] = -1;
   for (int h = 0; h < s.plan.nh; ++h) a.vmap[s.plan.h_v2[h]] = h;
-  for (int b = 0; b < s.plan.nb; ++b) {
-    a.b_plane[b] = s.plan.b_plane[b];
-    a.b_v0[b] = s.plan.b_v0[b];
-    a.b_g[b] = s.plan.b_g[b];
-    if (b + 1 == s.plan.nb || s.plan.b_g[b + 1] != s.plan.b_g[b]) a.b_end |= 1u << b;
+  // stage-1 groups whose blocks read the same (plane, x variant) set compute
+  // the same G (3D M+K: the two a12 blocks, θ/η = e2/e3 and e3/e2, both use
+  // the x variant 0): contract it once, let stage 2 read it for both
+  {
+    auto key = [&](int g) {
+      int k[kMaxBlocks], n = 0;
+      for (int b = s.plan.g_b0[g]; b < s.plan.g_b0[g] + s.plan.g_nb[g]; ++b)
+        k[n++] = s.plan.b_plane[b] * 4 + s.plan.b_v0[b];
+      std::sort(k, k + n);
+      long long h = n;
+      for (int i = 0; i < n; ++i) h = h * 1031 + k[i];
+      return h;
+    };
+    for (int g = 0; g < s.plan.ng; ++g) {
+      a.g_src[g] = g;
+      for (int q = 0; q < g; ++q)
+        if (a.g_src[q] == q && key(q) == key(g)) {
+          a.g_src[g] = q;
+          break;
+        }
+    }
+    int nb = 0;
+    for (int b = 0; b < s.plan.nb; ++b) {
+      const int g = s.plan.b_g[b];
+      if (a.g_src[g] != g) continue;
+      a.b_plane[nb] = s.plan.b_plane[b];
+      a.b_v0[nb] = s.plan.b_v0[b];
+      a.b_g[nb] = g;
+      ++nb;
+    }
+    a.nb1 = nb;
+    for (int b = 0; b < nb; ++b)
+      if (b + 1 == nb || a.b_g[b + 1] != a.b_g[b]) a.b_end |= 1u << b;
+    // halves at a group boundary, balanced by block count
+    a.half_b1 = nb;
+    int best = 1 << 30;
+    for (int b = 0; b + 1 < nb; ++b)
+      if ((a.b_end >> b) & 1) {
+        const int imb = std::abs(2 * (b + 1) - nb);
+        if (imb < best) {
+          best = imb;
+          a.half_b1 = b + 1;
+        }
+      }
   }
   for (int g = 0; g < s.plan.ng; ++g) {
     a.g_v1[g] = s.plan.g_v1[g];

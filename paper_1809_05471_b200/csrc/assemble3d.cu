@@ -22,6 +22,7 @@
 //         ring[m2][n2] += Σ_h W_z^{v2(h)} H_h  ->  CSR
 //   2D: asm2_stage1 (x) -> HBM, asm_sweep<2> (y ring, chunked) -> CSR.
 #include "fused.cuh"
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
