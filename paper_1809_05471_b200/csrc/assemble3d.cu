@@ -913,6 +913,7 @@ TabArgs tab_args(const igs_problem* p) {
 }
 
 #include "asm3_sym.cuh"
+#include "asm2_sym.cuh"
 
 // The one-pass symmetric kernel serves this problem (3D, p <= 4, A = Aᵀ).
 bool sym_eligible(const igs_problem* p, const AsmShape& s) {
@@ -1264,11 +1265,23 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
   }
   int64_t* base = reinterpret_cast<int64_t*>(ws);
   double* buf = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + 256);
-  row_start_kernel<<<1, 1, 0, st>>>(pat, row_lo, base);
-  IGS_LAUNCH_CHECK("row_start_kernel");
   const int P = s.fs.p, Q = s.fs.k;
   const bool ko = (flags & IGS_FLAG_KERNEL_ONLY) != 0;
   if (row_hi <= row_lo) return IGS_OK;
+  // 2D, whole matrix: the one-pass symmetric kernel (values start at row 0)
+  if (!(flags & IGS_FLAG_TWO_PASS) && sym2_eligible(p, s, row_lo, row_hi)) {
+    igs_status r = IGS_ECAPACITY;
+    switch (P) {
+      case 2: r = launch2_sym<2>(p, s, pat, planes, values, st); break;
+      case 3: r = launch2_sym<3>(p, s, pat, planes, values, st); break;
+      case 4: r = launch2_sym<4>(p, s, pat, planes, values, st); break;
+      case 5: r = launch2_sym<5>(p, s, pat, planes, values, st); break;
+      default: break;
+    }
+    if (r != IGS_ECAPACITY) return r;
+  }
+  row_start_kernel<<<1, 1, 0, st>>>(pat, row_lo, base);
+  IGS_LAUNCH_CHECK("row_start_kernel");
   if (sym_eligible(p, s) && !(flags & IGS_FLAG_TWO_PASS)) {
     const bool slab = p->slab_lo || p->slab_hi;
     const int sl = slab ? p->slab_lo : 0, sh = slab ? p->slab_hi : (int)s.fs.nel[2];

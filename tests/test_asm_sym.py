@@ -1,4 +1,4 @@
-"""The one-pass symmetric 3D assembly (csrc/asm3_sym.cuh) against the oracle.
+"""The one-pass symmetric assemblies (csrc/asm3_sym.cuh, csrc/asm2_sym.cuh) against the oracle.
 
 For symmetric problems (trial == test, first-order sets, F_{η,θ} = F_{θ,η})
 the fused 3D assembly (asm3_sym) forms only the x-pairs with n0 >= m0 and writes each
@@ -47,6 +47,12 @@ def _rel(a, b):
 @pytest.mark.parametrize("p,K,kind", [
     (4, (1, 1, 1), 3), (4, (2, 5, 1), 3), (4, (5, 3, 9), 2), (4, (9, 6, 3), 3), (4, (7, 7, 7), 1),
     (4, (13, 4, 6), 3), (4, (17, 9, 5), 2), (2, (13, 21, 2), 3), (2, (1, 3, 5), 1), (2, (8, 10, 9), 2),
+    # 2D (asm2_sym: x strips sweeping y in chunks): tiny, ragged strips,
+    # many chunks, all orders 2..5, mass / stiffness / mass+stiffness
+    # (x points p·K0 even: the TMA row pitch must be a 16-byte multiple)
+    (5, (2, 1), 2), (5, (2, 7), 3), (5, (20, 5), 2), (5, (38, 23), 3), (5, (40, 37), 2), (5, (64, 96), 2),
+    (4, (1, 6), 1), (4, (24, 25), 3), (4, (31, 50), 2), (3, (64, 64), 1), (3, (34, 9), 3), (3, (70, 41), 2),
+    (2, (48, 10), 3), (2, (50, 3), 1), (2, (97, 61), 2),
 ])
 def test_sym_assembly_vs_oracle_and_two_pass(cuda, p, K, kind):
     sumfac, workloads = _mods()
