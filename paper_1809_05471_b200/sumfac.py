@@ -357,33 +357,46 @@ def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
     else:
         ip = pat.indptr
         n_out = int(ip[hi] - ip[lo])
-    # the fused kernels write every entry of the range (band zeros included)
-    fused = (block is None and not (flags & _lib.FLAG_FORCE_GENERIC)
-             and lib.igs_fused_path(ctypes.byref(prob), _lib.OP_ASSEMBLE))
-    values = (torch.empty if fused else torch.zeros)(n_out, dtype=torch.float64, device="cuda")
-    if n_out == 0:
-        return values
-    ws_bytes = lib.igs_workspace_bytes(ctypes.byref(prob), _lib.OP_ASSEMBLE, flags)
-    ws = problem._cache.get(("ws_asm", ws_bytes))
-    if ws is None:
-        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
-        problem._cache[("ws_asm", ws_bytes)] = ws
-    d = problem.d
-    rp = (ctypes.c_void_p * 3)(*[dp.rowptr_dev.data_ptr() for dp in pat.dir_pairs] + [0] * (3 - d))
-    cl = (ctypes.c_void_p * 3)(*[dp.cols_dev.data_ptr() for dp in pat.dir_pairs] + [0] * (3 - d))
-    bi, bj = block if block is not None else (-1, -1)
-    f = problem.coeff_field()
-    st = lib.igs_assemble_values(ctypes.byref(prob), rp, cl, lo, hi, bi, bj, _lib.ptr(f.planes),
-                                 _lib.ptr(values), _lib.ptr(ws), ws_bytes, flags, _lib.stream_handle())
-    _lib.check(st, "assemble_values")
-    if counter is not None:
+    # per-(block, dir_order, flags) launch data, cached on the problem like the
+    # reference's lazily built tables/core (sumfac.py:296-337): the fused-path
+    # test, the workspace, the 1D pattern pointer arrays and the analytic
+    # FlopCounter increments (warm calls then cost one C-ABI call)
+    key = ("asm_launch", block, None if dir_order is None else tuple(dir_order), flags)
+    lc = problem._cache.get(key)
+    if lc is None:
+        fused = bool(block is None and not (flags & _lib.FLAG_FORCE_GENERIC)
+                     and lib.igs_fused_path(ctypes.byref(prob), _lib.OP_ASSEMBLE))
+        ws_bytes = lib.igs_workspace_bytes(ctypes.byref(prob), _lib.OP_ASSEMBLE, flags)
+        ws = problem._cache.get(("ws_asm", ws_bytes))
+        if ws is None:
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda")
+            problem._cache[("ws_asm", ws_bytes)] = ws
+        d = problem.d
+        rp = (ctypes.c_void_p * 3)(*[dp.rowptr_dev.data_ptr() for dp in pat.dir_pairs] + [0] * (3 - d))
+        cl = (ctypes.c_void_p * 3)(*[dp.cols_dev.data_ptr() for dp in pat.dir_pairs] + [0] * (3 - d))
+        bi, bj = block if block is not None else (-1, -1)
+        f = problem.coeff_field()
+        updates = 0
         for j, th in enumerate(problem.theta_set):
             for i, et in enumerate(problem.eta_set):
                 if block is not None and (i, j) != (bi, bj):
                     continue
                 if f.is_zero_block(i, j):
                     continue
-                counter.add_block_update(block_update_count(problem, th, et, dir_order))
+                updates += block_update_count(problem, th, et, dir_order)
+        lc = (fused, ws_bytes, ws, rp, cl, bi, bj, updates)
+        problem._cache[key] = lc
+    fused, ws_bytes, ws, rp, cl, bi, bj, updates = lc
+    # the fused kernels write every entry of the range (band zeros included)
+    values = (torch.empty if fused else torch.zeros)(n_out, dtype=torch.float64, device="cuda")
+    if n_out == 0:
+        return values
+    f = problem.coeff_field()
+    st = lib.igs_assemble_values(ctypes.byref(prob), rp, cl, lo, hi, bi, bj, _lib.ptr(f.planes),
+                                 _lib.ptr(values), _lib.ptr(ws), ws_bytes, flags, _lib.stream_handle())
+    _lib.check(st, "assemble_values")
+    if counter is not None:
+        counter.add_block_update(updates)
     return values
 
 
