@@ -114,7 +114,7 @@ struct SymArgs {
   TabArgs tab;
   TensorPat pat;
   double* values;
-  const int64_t* base;   // CSR offset of row_lo (device scalar)
+  const int64_t* base;   // CSR offset of row_lo (device scalar; null: row_lo = 0, offset 0)
   int64_t row_lo, row_hi;
   int nt0;               // tiles in x
   int nplanes;
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(512, 1)
   const int64_t dBase = dA * W + dC;
   const int64_t mBase = mA * W + mC + (int64_t)(2 * P - 2) * mD - P01 * W * (P - 1);
   const int64_t mStep = P01 * W - mD;
-  const int64_t base = *a.base;
+  const int64_t base = a.base ? *a.base : 0;
   const int64_t m_flat0 = m0 + N0 * m1, n_flat0 = n0 + N0 * n1;
   // z-row table of the rows this chunk completes or mirrors into
   const int zr0 = max(0, e_lo - (P - 1));

@@ -1280,20 +1280,31 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
     }
     if (r != IGS_ECAPACITY) return r;
   }
-  row_start_kernel<<<1, 1, 0, st>>>(pat, row_lo, base);
-  IGS_LAUNCH_CHECK("row_start_kernel");
+  // the CSR offset of row_lo (device scalar in the workspace, written by a
+  // one-thread kernel; the one-pass kernel needs none for ranges at row 0)
+  bool base_set = false;
+  auto set_base = [&]() -> igs_status {
+    if (base_set) return IGS_OK;
+    base_set = true;
+    row_start_kernel<<<1, 1, 0, st>>>(pat, row_lo, base);
+    IGS_LAUNCH_CHECK("row_start_kernel");
+    return IGS_OK;
+  };
   if (sym_eligible(p, s) && !(flags & IGS_FLAG_TWO_PASS)) {
     const bool slab = p->slab_lo || p->slab_hi;
     const int sl = slab ? p->slab_lo : 0, sh = slab ? p->slab_hi : (int)s.fs.nel[2];
+    if (row_lo != 0) IGS_TRY(set_base());
+    const int64_t* sb = row_lo != 0 ? base : nullptr;
     igs_status r = IGS_ECAPACITY;
     switch (P) {
-      case 2: r = launch3_sym<2>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
-      case 4: r = launch3_sym<4>(p, s, pat, row_lo, row_hi, base, planes, values, sl, sh, st); break;
+      case 2: r = launch3_sym<2>(p, s, pat, row_lo, row_hi, sb, planes, values, sl, sh, st); break;
+      case 4: r = launch3_sym<4>(p, s, pat, row_lo, row_hi, sb, planes, values, sl, sh, st); break;
       default: break;
     }
     if (r != IGS_ECAPACITY) return r;  // else: the slab lacks the kernel's halo, two-pass below
   }
   if (ws_bytes < asm_workspace(s)) return fail(IGS_EWORKSPACE, "workspace too small for the fused assembly");
+  IGS_TRY(set_base());
   igs_status r = IGS_ECAPACITY;
   bool done = false;
 #define IGS_ASM_CASE(PP, QQ)                                                                    \

@@ -1,11 +1,20 @@
-import sys, torch
+"""One cold and one warm assembly of a BASELINE config (profiling target);
+the warm call is bracketed by cudaProfilerStart/Stop so
+`ncu --profile-from-start off` sees only its launches."""
+import sys
+
+import torch
+
 sys.path.insert(0, ".")
-from paper_1809_05471_b200 import sumfac, workloads
+from paper_1809_05471_b200 import sumfac, workloads  # noqa: E402
+
 name = sys.argv[1]
 c = workloads.CONFIGS[name]
 prob = workloads.make_problem(c["d"], c["p"], c["K"], c["kind"])
 A = sumfac.assemble(prob)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
 A = sumfac.assemble(prob)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", A.nnz)
