@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   double* Tw = Yr + C::YR;      // [NWIN][4][32 lanes][2]  window table fragments
   double* Ty = Tw + C::TBX;     // [EY][2][8][8]
   double* Tzb = Ty + C::TBY;    // [2 buffers][2][8][8]
-  double* Wx = Tzb + C::TBZ;    // [TX]
+  double* Wx = Tzb + C::TBZ;    // [TX] (unused: w_x lives in the X^T window tables)
   double* Wy = Wx + TX;         // [TY]
   double* Wzb = Wy + TY;        // [2 buffers][8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(Wzb + 16);  // [NW][STG]
@@ -312,8 +312,11 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     const int c = kp < 2 ? lm + 4 * s : C::ROT ? ((lg - C::c0w(w)) & 7) : lg, pt = kp < 2 ? lg : 2 * lm + s;
     const int el = (8 * w + pt) / Q, j = (8 * w) / Q + c - el, ge = ex0 + el;
     double val = 0.0;
-    if (ge < a.K0 && j >= 0 && j < P && (v == 0 || STIFF))
-      val = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + (int64_t)ex0 * Q + 8 * w + pt];
+    if (ge < a.K0 && j >= 0 && j < P && (v == 0 || STIFF)) {
+      const int64_t x = (int64_t)ex0 * Q + 8 * w + pt;
+      val = a.vals[0][((int64_t)v * P + j) * a.xtab[0] + x];
+      if (kp >= 2) val *= a.wts[0][x];  // test side: the x quadrature weight folded in
+    }
     Tw[i] = val;
   }
   for (int i = tid; i < EY * 2 * Q * P; i += NT) {
@@ -321,10 +324,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     int ge = ey0 + e;
     if (ge < a.K1)
       Ty[((e * 2 + v) * 8 + q) * 8 + j] = a.vals[1][((int64_t)v * P + j) * a.xtab[1] + (int64_t)ge * Q + q];
-  }
-  for (int i = tid; i < TX; i += NT) {
-    int64_t gg = (int64_t)ex0 * Q + i;
-    if (gg < a.X0) Wx[i] = a.wts[0][gg];
   }
   for (int i = tid; i < TY; i += NT) {
     int64_t gg = (int64_t)ey0 * Q + i;
@@ -347,10 +346,11 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     const int line = wlg * 8 + g, eyl = line / Q, q1 = line % Q, jj = ynb + m + 4 * s - eyl;
     return (jj >= 0 && jj < P && (v == 0 || STIFF)) ? Ty[((eyl * 2 + v) * 8 + q1) * 8 + jj] : 0.0;
   };
-  // transpose: A[k = g][line' = m + 4s] = By_v[line' % Q][ynb + g - line' / Q]
+  // transpose: A[k = g][line' = m + 4s] = w_y(line')·By_v[line' % Q][ynb + g - line' / Q]
+  // (test side: the y quadrature weight folded in; zero past the mesh)
   auto yt_frag = [&](int v, int s) {
     const int lt = wlg * 8 + m + 4 * s, eyt = lt / Q, qt = lt % Q, jt = ynb + g - eyt;
-    return (jt >= 0 && jt < P && (v == 0 || STIFF)) ? Ty[((eyt * 2 + v) * 8 + qt) * 8 + jt] : 0.0;
+    return (jt >= 0 && jt < P && (v == 0 || STIFF)) ? Ty[((eyt * 2 + v) * 8 + qt) * 8 + jt] * Wy[lt] : 0.0;
   };
   __syncthreads();
   for (int n1 = tid; n1 < FY; n1 += NT) {
@@ -393,7 +393,8 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   // Z^T of the Q2B point layers of batch `b` into the y ring (item mapping
   // (n1, n0) identical in every phase that touches the ring).  S row n1 is
   // the fixed-order sum of the partials of line groups zr[n1] = lo | hi << 8.
-  auto zt_item = [&](const double* Tz, int e2, int b, int i) {
+  // The z quadrature weight of point layer q2 scales its partials (test side).
+  auto zt_item = [&](const double* Tz, const double* Wzp, int e2, int b, int i) {
     const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
     const int lr = zr[n1], lo = lr & 255, hi = lr >> 8;
     double s0[Q2B], s1[Q2B];
@@ -405,8 +406,9 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
         a0 += sp[0];
         if (STIFF) a1 += sp[CQL];
       }
-      s0[qb] = a0;
-      s1[qb] = a1;
+      const double wz = Wzp[b * Q2B + qb];
+      s0[qb] = a0 * wz;
+      s1[qb] = a1 * wz;
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       PHASE_MARK(0);  // element setup / previous batch tail
       // ---- Z^T(previous batch) + Z(this batch) + clear S ---------------------
       if (b > 0)
-        for (int i = tid; i < FY * FX; i += NT) zt_item(Tz, e2, b - 1, i);
+        for (int i = tid; i < FY * FX; i += NT) zt_item(Tz, Wz, e2, b - 1, i);
       for (int i = tid; i < Q2B * FY * FX; i += NT) {
         const int qb = i / (FY * FX), r = i % (FY * FX);
         const int n0 = r % FX, n1 = r / FX, o = n1 * RP + n0;
@@ -458,7 +460,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
       PHASE_MARK(1);  // Z (+ Z^T of the previous batch)
       // ---- Y (DMMA), X (DMMA) + pointwise + X^T (DMMA): warp-private rows -----
       {
-        const int q2 = b * Q2B + wq;
         const int line = wlg * 8 + g;   // A-fragment / D row
         double* Cb = Cq + wq * NV * CQL;
         double* Crow = Cb + line * RP;  // C (then R) row of this lane's line
@@ -498,8 +499,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           __syncwarp();
         }
         PHASE_MARK(2);  // Y
-        const bool line_ok = (ey0 + line / Q) < a.K1;
-        const double wyz = Wz[q2] * Wy[line];
         const int widx0 = widx;         // = batch·NBX
         // point layers (slab-local) of this batch's and the next batch's boxes
         const int zq_cur = e2 * Q + b * Q2B + wq;
@@ -541,7 +540,6 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           cf[1][s] = STIFF ? Crow[CQL + m + 4 * s] : 0.0;
           cf[2][s] = STIFF ? Crow[2 * CQL + m + 4 * s] : 0.0;
         }
-        const double wl = line_ok ? wyz : 0.0;
 #pragma unroll
         for (int w = 0; w < NWIN; ++w) {
           const int c0 = C::c0w(w);
@@ -598,19 +596,19 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
             ld2(p02, fv[5]);
             ld2(p12, fv[6]);
           }
-          // pointwise (the x weight is zero past the mesh)
+          // pointwise g = F·∇u (the quadrature weights w_x, w_y, w_z are
+          // folded into the test-side tables of X^T, Y^T and Z^T; they are
+          // zero past the mesh, which masks the finite values read there)
           double g0[2], gx[2], gy[2], gz[2];
-          const double2 wx2 = *reinterpret_cast<const double2*>(Wx + 8 * w + 2 * m);
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const double wt = wl * (c == 0 ? wx2.x : wx2.y);
-            if (MASS) g0[c] = wt * (fv[0][c] * u[c]);
+            if (MASS) g0[c] = fv[0][c] * u[c];
             if (STIFF) {
               const double f00 = fv[1][c], f11 = fv[2][c], f22 = fv[3][c];
               const double f01 = fv[4][c], f02 = fv[5][c], f12 = fv[6][c];
-              gx[c] = wt * fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
-              gy[c] = wt * fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
-              gz[c] = wt * fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
+              gx[c] = fma(f00, ux[c], fma(f01, uy[c], f02 * uz[c]));
+              gy[c] = fma(f01, ux[c], fma(f11, uy[c], f12 * uz[c]));
+              gz[c] = fma(f02, ux[c], fma(f12, uy[c], f22 * uz[c]));
             }
           }
           // transpose into the window: W^T[line][c] += Σ_pt g^T[line][pt] · B[pt][c]
@@ -748,7 +746,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
     PHASE_MARK(4);  // Y^T of the last batch
     // last Z^T of the element, flush DoF layer e2 (complete for this chunk)
     for (int i = tid; i < FY * FX; i += NT) {
-      zt_item(Tz, e2, NB - 1, i);
+      zt_item(Tz, Wz, e2, NB - 1, i);
       const int n0 = i % FX, n1 = i / FX, o = n1 * RP + n0;
       double* yr = Yr + (e2 % P) * LXR + o;
       box[(int64_t)(e2 - z0) * FY * FX + i] = *yr;
