@@ -275,7 +275,11 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
   uint64_t* mybar = bars + warp * STG;
   double* mystage = Fs + warp * STG * FST;
   // one lane: box of window bx of point layer zq into ring stage stg
+#ifdef IGS_DEV_SWITCHES
   const bool co = a.l2pf < 0;  // compute-only measurement mode
+#else
+  constexpr bool co = false;
+#endif
   const int tma_x = ex0 * Q, tma_y = ey0 * Q + wlg * 8;
   auto issue_box = [&](int stg, int bx, int zq) {
     uint64_t* bar = mybar + stg;
@@ -401,11 +405,14 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
 #pragma unroll
     for (int qb = 0; qb < Q2B; ++qb) {
       double a0 = 0.0, a1 = 0.0;
-      for (int lg = lo; lg <= hi; ++lg) {
-        const double* sp = Cq + qb * NV * CQL + (lg * 8 + n1 - (lg * 8) / Q) * RP + n0;
-        a0 += sp[0];
-        if (STIFF) a1 += sp[CQL];
-      }
+      // line group lg's partial of DoF row n1 sits in row lg·8 + n1 - lg·8/Q
+      const double* sp = Cq + qb * NV * CQL + n1 * RP + n0;
+#pragma unroll
+      for (int lg = 0; lg < NLG; ++lg)
+        if (lg >= lo && lg <= hi) {
+          a0 += sp[(lg * 8 - (lg * 8) / Q) * RP];
+          if (STIFF) a1 += sp[(lg * 8 - (lg * 8) / Q) * RP + CQL];
+        }
       const double wz = Wzp[b * Q2B + qb];
       s0[qb] = a0 * wz;
       s1[qb] = a1 * wz;
