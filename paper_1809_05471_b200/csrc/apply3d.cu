@@ -141,6 +141,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// (A suspend-time hint on try_wait was measured 3 % slower over BASELINE's
+// 100 sustained applies: the wake-up latency costs more than the spin.)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
@@ -643,7 +645,10 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           // or slide the accumulator window by d columns
           const int d = (w + 1 < NWIN ? C::c0w(w + 1) : c0 + 8) - c0;
           if (w + 1 < NWIN) {
-            __syncwarp();
+            // (ROT: every lane's reads of these C columns fed the forward
+            // MMAs, whose results the transposed MMAs consumed before the
+            // __syncwarp above)
+            if constexpr (!C::ROT) __syncwarp();
             if constexpr (C::ROT) {
 #pragma unroll
               for (int c = 0; c < 2; ++c) {
