@@ -53,9 +53,29 @@ def asm_row(p, kind, K=64, reps=5):
     torch.cuda.empty_cache()
 
 
+def asm2_row(p, kind, K=256, reps=10):
+    prob = workloads.make_problem(2, p, K, kind, max_nnz=1 << 40)
+    A = sumfac.assemble(prob)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        A = sumfac.assemble(prob)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print(f"assemble2d p={p} kind={'K' if kind == 2 else 'M+K'} 256^2: {ms:8.3f} ms  {A.nnz / ms / 1e6:6.2f} G nnz/s  "
+          f"nnz {A.nnz}  fused={sumfac.fused_path(prob)}", flush=True)
+    del prob, A
+    torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
+    # small assemblies first (the large apply problems fragment the allocator)
+    for p in range(2, 7):
+        asm2_row(p, 2)
+    for p in range(2, 7):
+        asm_row(p, 3)
     for kind in (2, 3):
         for p in range(2, 9):
             apply_row(p, kind)
-    for p in range(2, 7):
-        asm_row(p, 3)

@@ -58,6 +58,11 @@ def case(d, p, K, kind, reps=50):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "orders":
+        for p in range(2, 7):
+            o = case(2, p, 256, 2, reps=10)
+            print(p, json.dumps({k: o[k] for k in ("one_graph_ms", "one_loop_ms", "two_graph_ms", "rel_one_vs_two")}))
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "c2":
         o = case(2, 5, 256, 2)
         print(sys.argv[2:] or "", json.dumps({k: o[k] for k in ("one_graph_ms", "two_graph_ms", "rel_one_vs_two")}))
