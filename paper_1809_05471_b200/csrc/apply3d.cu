@@ -204,6 +204,9 @@ struct Cfg {
   // load their own rotated table instead of sharing a hoisted one (measured:
   // C4 3.84 -> 3.75 ms, C5 11.3 -> 10.9 ms).  IGS_APPLY_ROT=0 (measurement
   // builds) restores the sliding window.
+#ifndef IGS_APPLY_SYNCWARP
+#define IGS_APPLY_SYNCWARP 0
+#endif
 #ifndef IGS_APPLY_ROT
   static constexpr bool ROT = true;
 #else
@@ -630,9 +633,13 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
               dmma(w01[0], w01[1], gz[s], tb0[s]);
             }
           }
-          // every lane's reads of this stage have been consumed (the MMAs above
-          // depend on them): hand the stage to the next box of this warp
+          // every lane's reads of this stage have been consumed: the
+          // transposed MMAs above (warp-synchronous mma.sync) consumed every
+          // lane's g, which needed its coefficient loads; hand the stage to
+          // the next box of this warp
+#if IGS_APPLY_SYNCWARP
           __syncwarp();
+#endif
           if (lane == 0 && widx0 + w + STG < ntask) {
             // box w + STG of this row: window (w + STG) % NBX of this or the next batch
             const int nxt = w + STG;
@@ -646,8 +653,7 @@ __global__ void __launch_bounds__(Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG_>::NT,
           const int d = (w + 1 < NWIN ? C::c0w(w + 1) : c0 + 8) - c0;
           if (w + 1 < NWIN) {
             // (ROT: every lane's reads of these C columns fed the forward
-            // MMAs, whose results the transposed MMAs consumed before the
-            // __syncwarp above)
+            // MMAs, which every lane passed before the transposed MMAs)
             if constexpr (!C::ROT) __syncwarp();
             if constexpr (C::ROT) {
 #pragma unroll

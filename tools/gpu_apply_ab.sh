@@ -1,4 +1,4 @@
-for r in 1 2 3 4; do
+for r in 1 2 3; do
 for c in C4 C5; do
 for v in variants/*/ new; do
  if [ $v = new ]; then python tools/time_apply.py $c | sed "s/^/new /"; else IGS_LIB_PATH=$v/libigs_b200.so python tools/time_apply.py $c | sed "s|^|$v |"; fi
