@@ -888,7 +888,9 @@ bool pick(int P, int Q, Launch* L) {
     // p = 4: 8-row y tiles (16 warps) where they fit shared memory (measured
     // 1.51 -> 1.21 ms at 128^3, stiffness), else 4-row tiles (mass+stiffness)
     case 2: *L = make_launch<2, 2, 8, 8, 2, MASS, STIFF>(); return true;
-    case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF>(); return true;
+    // p = 3: a single TMA stage lets two CTAs share an SM (18 warps):
+    // 0.73 -> 0.66 ms at 128^3 (stiffness)
+    case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF, 1>(); return true;
     case 4:
       *L = make_launch<4, 4, 8, 8, 4, MASS, STIFF>();
       if (L->smem > 232448) *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>();
@@ -898,7 +900,13 @@ bool pick(int P, int Q, Launch* L) {
       if (apply_variant() == 1 || (MASS && STIFF)) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
       else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
       return true;
-    case 7: *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>(); return true;
+    // p = 7: stiffness on a single TMA stage (two CTAs per SM: 7.35 ->
+    // 6.45 ms at 128^3), mass+stiffness on three (8.0 -> 7.7 ms)
+    case 7:
+      if (MASS && STIFF) *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF, 3>();
+      else if (STIFF) *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF, 1>();
+      else *L = make_launch<7, 7, 8, 8, 1, MASS, STIFF>();
+      return true;
     case 8:
       if (apply_variant() == 1) *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 4>();
       else if (apply_variant() == 2) *L = make_launch<8, 8, 8, 2, 2, MASS, STIFF, 2>();
