@@ -338,7 +338,7 @@ def block_update_count(problem, theta, eta, dir_order=None):
     return total
 
 
-def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
+def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None, out=None):
     """Values of rows [lo, hi) (default: all) in CSR order.  With a slab
     coefficient field (elements [slab_lo, slab_hi) of the last direction,
     SURVEY §8(e)) the rows must only need slab elements; the result then
@@ -388,7 +388,15 @@ def _run_assembly(problem, block, counter, dir_order, flags=0, row_range=None):
         problem._cache[key] = lc
     fused, ws_bytes, ws, rp, cl, bi, bj, updates = lc
     # the fused kernels write every entry of the range (band zeros included)
-    values = (torch.empty if fused else torch.zeros)(n_out, dtype=torch.float64, device="cuda")
+    if out is not None:
+        # caller-provided value storage (contiguous float64 CUDA, >= n_out entries)
+        if out.dtype != torch.float64 or out.device.type != "cuda" or not out.is_contiguous() or out.numel() < n_out:
+            raise ValueError(f"out must be a contiguous float64 CUDA tensor with >= {n_out} entries")
+        values = out.reshape(-1)[:n_out]
+        if not fused:
+            values.zero_()
+    else:
+        values = (torch.empty if fused else torch.zeros)(n_out, dtype=torch.float64, device="cuda")
     if n_out == 0:
         return values
     f = problem.coeff_field()
