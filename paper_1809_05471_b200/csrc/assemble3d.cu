@@ -653,6 +653,149 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
   }
 }
 
+// ---- 3D three-pass path (orders whose stage-1/2 tile would be < 4 rows) ---
+//
+// At p >= 5 the fused stage-1/2 kernel only fits 2 x 2 (p = 5) or 1 x 1
+// (p = 6) row tiles: every tile re-reads and re-contracts a (T+p-1)^2 region
+// for T^2 rows (9x / 36x redundant) and its MMA tiles are nearly empty.  The
+// three-pass path splits the two contractions (the reference's recursion,
+// sumfac.py:200-213, one direction per pass):
+//   pass A  asm2_stage1 over the rows (y, z) of a chunk of z layers:
+//           G_g[(z,y)][s0] = Σ_{b∈g} Σ_x F_b W0^{v0(b)}            (DMMA, -> HBM chunk)
+//   pass B  asm_ysweep: one thread per (s0, z, stage-2 group h) sweeps y with
+//           the ring of P rows x (2P-1) columns of asm_sweep, exact band
+//           sparsity on DFMA:  H_h[s1][s0] = Σ_{g∈h} Σ_y W1^{v1(g)} G_g  -> HBM
+//   pass C  asm_sweep<3> (z), as for the two-pass path.
+struct AsmYArgs {
+  TabArgs tab;
+  const double* G;      // chunk, sweep-blocked [NS0 blocks][layer·K1 + e1][Q][ng][128]
+  double* H;            // sweep-blocked [pair blocks][e2 - e_lo][Q][nh][128]
+  const double* w1g;    // per y element: separable factors [Q][wB^0 | wB^1 | B^0 | B^1][PP] (+ 4 unused)
+  int64_t NS0;
+  int64_t NE_G;         // layers in the chunk x K1
+  int64_t zrel0;        // z point of the chunk's first layer relative to H's first point
+  int64_t NE_H;
+  int ng, nh;
+  int h_g0[4], h_ng[4];
+  int vmap[4][4];       // [h][v1]: group (relative to h_g0[h]) holding y variant v1, -1: none
+};
+
+template <int P, int Q>
+__global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs a) {
+  using C = S3Cfg<P, Q>;
+  constexpr int W = 2 * P - 1, NWT = C::NWT, NWR = C::NWR, PP = C::PP;
+  extern __shared__ __align__(16) double s3[];
+  double* hst = s3;                    // [NS3][Q][hng][NT3]
+  double* w2s = s3 + NS3 * C::HST;     // [NS3][NWR]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWR);
+  const int tid = threadIdx.x;
+  const int64_t sb = blockIdx.x;
+  const int zl = blockIdx.y, h = blockIdx.z;
+  const int hng = a.h_ng[h], g0 = a.h_g0[h];
+  const int64_t s0 = sb * NT3 + tid;
+  const bool valid = s0 < a.NS0;
+  const int K1 = a.tab.K[1];
+  const int64_t zrel = a.zrel0 + zl;
+  const int64_t ez = zrel / Q;
+  const int qz = (int)(zrel % Q);
+  int vm[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) vm[v] = a.vmap[h][v];
+  double ring[P][W];
+#pragma unroll
+  for (int r = 0; r < P; ++r)
+#pragma unroll
+    for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
+  // row m1 is final: its 2P-1 slots s1 = m1·W + k of this thread's s0
+  auto flush = [&](int64_t m1, const double* row) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int64_t sp = (m1 * W + k) * a.NS0 + s0;
+      a.H[sweep_offset(sp, ez, qz, h, a.NE_H, Q, a.nh)] = row[k];
+    }
+  };
+  const unsigned qbytes = (unsigned)(hng * NT3 * sizeof(double));
+  const unsigned wbytes = (unsigned)(NWR * sizeof(double));
+  const double* gblock = a.G + ((sb * a.NE_G + (int64_t)zl * K1) * Q * a.ng + g0) * NT3;
+  auto issue = [&](int e1) {  // one thread
+    if (e1 >= K1) return;
+    const int stg = e1 % NS3;
+    dev::mbar_expect_tx(bars + stg, Q * qbytes + wbytes);
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      dev::bulk_load(hst + stg * C::HST + q * hng * NT3, gblock + ((int64_t)e1 * Q + q) * a.ng * NT3, qbytes,
+                     bars + stg);
+    dev::bulk_load(w2s + stg * NWR, a.w1g + (int64_t)e1 * NWR, wbytes, bars + stg);
+  };
+  if (tid < NS3) dev::mbar_init(bars + tid, 1);
+  dev::fence_mbar_init();
+  __syncthreads();
+  if (tid == 0)
+    for (int e = 0; e < D3; ++e) issue(e);
+  for (int eb = 0; eb < K1; eb += P) {
+#pragma unroll
+    for (int r = 0; r < P; ++r) {  // ring row of element e1 is static: r
+      const int e1 = eb + r;
+      if (e1 >= K1) break;
+      __syncthreads();  // stage (e1 + D3) % NS3 was last read for element e1 - 1
+      if (tid == 0) {
+        dev::fence_proxy_async();
+        issue(e1 + D3);
+      }
+      const int stg = e1 % NS3;
+      dev::mbar_wait(bars + stg, (unsigned)((e1 / NS3) & 1));
+      const double* hcol = hst + stg * C::HST + tid;
+      const double* wst = w2s + stg * NWR;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        double hv[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) hv[v] = vm[v] >= 0 ? hcol[(q * hng + vm[v]) * NT3] : 0.0;
+        double fb[4][P];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int j = 0; j < P; j += 2) {
+            if (j + 1 < P) {
+              const double2 t = *reinterpret_cast<const double2*>(wst + (q * 4 + f) * PP + j);
+              fb[f][j] = t.x;
+              fb[f][j + 1] = t.y;
+            } else {
+              fb[f][j] = wst[(q * 4 + f) * PP + j];
+            }
+          }
+        double u0[P], u1[P];
+#pragma unroll
+        for (int jn = 0; jn < P; ++jn) {
+          u0[jn] = fma(fb[1][jn], hv[1], fb[0][jn] * hv[0]);
+          u1[jn] = fma(fb[1][jn], hv[3], fb[0][jn] * hv[2]);
+        }
+#pragma unroll
+        for (int jm = 0; jm < P; ++jm)
+#pragma unroll
+          for (int jn = 0; jn < P; ++jn) {
+            double& acc = ring[(r + jm) % P][jn - jm + P - 1];
+            acc = fma(fb[3][jm], u1[jn], fma(fb[2][jm], u0[jn], acc));
+          }
+      }
+      if (valid) flush(e1, ring[r]);
+#pragma unroll
+      for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
+    }
+  }
+  // trailing rows m1 in [K1, K1 + P - 1)
+  if (valid) {
+#pragma unroll
+    for (int t = 1; t < P; ++t) {
+      const int64_t m1 = K1 - 1 + t;
+      const int slot = (int)(m1 % P);
+#pragma unroll
+      for (int s = 0; s < P; ++s)
+        if (s == slot) flush(m1, ring[s]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- 2D -------
 
 struct Asm2Args {
@@ -662,8 +805,11 @@ struct Asm2Args {
   int64_t NS0;
   int64_t NE;      // elements of the last direction (K1)
   int nt0;         // row tiles in x
-  int yc;          // y points per CTA (multiple of A2_YS)
+  int yc;          // y points per CTA (multiple of the TMA box height YS)
   const double* Wg;  // [nt0][W0T] band tables, built once per assembly (asm2_tables_kernel)
+  int64_t X1;      // rows (y points) to contract: 2D the y points; 3D three-pass a chunk of
+                   // z layers flattened with y (row = zl·X1d + y, NE = layers·K1)
+  int64_t ytma0;   // TMA row of row 0 (3D three-pass: the chunk's first layer; 2D: 0)
 };
 
 // The 2D tiles' band tables, one block per row tile, built once per
@@ -682,18 +828,19 @@ __global__ void asm2_tables_kernel(const TabArgs tab, double* Wg) {
 // boxes of A2_YS y rows x the tile's x region (all planes) stream in by
 // TMA, double-buffered.  G_g[y][s0] = Σ_{b∈g} Σ_x F_b[y][x] W0^{v0(b)}[x][s0].
 constexpr int A2_YS = 64, A2_NT = 512, A2_NW = 16;
-template <int P, int Q, int T>
+template <int P, int Q, int T, int YS = A2_YS>
 struct A2Cfg {
   using B = A3Cfg<P, Q, T>;
-  static constexpr size_t fbox(int npl) { return ((size_t)npl * A2_YS * B::XR + 4 + 15) & ~size_t(15); }
+  static constexpr size_t fbox(int npl) { return ((size_t)npl * YS * B::XR + 4 + 15) & ~size_t(15); }
   static constexpr size_t smem(int npl) { return (2 * fbox(npl) + B::W0T) * sizeof(double) + 32; }
 };
 
-template <int P, int Q, int T>
+template <int P, int Q, int T, int YS = A2_YS>
 __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __grid_constant__ CUtensorMap fmap,
                                                      int nplanes) {
   using C = A3Cfg<P, Q, T>;
-  using C2 = A2Cfg<P, Q, T>;
+  using C2 = A2Cfg<P, Q, T, YS>;
+  constexpr int A2_YS = YS;  // (shadows the 2D default inside this kernel)
   constexpr int PT = C::PT, PTP = C::PTP, XR = C::XR, XK = C::XK, SP = C::SP, W = C::W, SR = C::SR;
   constexpr int KL = max_ksteps<P, Q, T>(PTP / 8, XK / 4);
   constexpr int NYB = A2_YS / 8, NST = PTP / 8;
@@ -707,7 +854,7 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
   const int g8 = lane >> 2, m4 = lane & 3;
   const int a0 = (blockIdx.x % a.nt0) * T;
   const int xb0 = (a0 - (P - 1)) * Q;
-  const int64_t X1 = a.tab.X[1];
+  const int64_t X1 = a.X1;
   const int64_t y_lo = (int64_t)(blockIdx.x / a.nt0) * a.yc;
   const int64_t y_hi = min64(X1, y_lo + a.yc);
   const int nstage = (int)((y_hi - y_lo + A2_YS - 1) / A2_YS);
@@ -726,7 +873,7 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
     }
     for (int i = 0; i < 2 && i < nstage; ++i) {
       dev::mbar_expect_tx(bar + i, fbytes);
-      dev::tma_load_4d(Fs + i * fb, &fmap, bar + i, xb0, (int)(y_lo + i * A2_YS), 0, 0);
+      dev::tma_load_4d(Fs + i * fb, &fmap, bar + i, xb0, (int)(a.ytma0 + y_lo + i * A2_YS), 0, 0);
     }
   }
   if (a.Wg) {
@@ -773,7 +920,7 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
     if (tid == 0 && i + 2 < nstage) {
       dev::fence_proxy_async();
       dev::mbar_expect_tx(bar + buf, fbytes);
-      dev::tma_load_4d(Fs + buf * fb, &fmap, bar + buf, xb0, (int)(y0 + 2 * A2_YS), 0, 0);
+      dev::tma_load_4d(Fs + buf * fb, &fmap, bar + buf, xb0, (int)(a.ytma0 + y0 + 2 * A2_YS), 0, 0);
     }
   }
 }
@@ -858,6 +1005,7 @@ struct AsmShape {
   FusedShape fs;
   AsmPlan plan;
   int64_t zpts;  // z points held by the coefficient planes (slab or grid)
+  int nplanes;
 };
 
 bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
@@ -883,6 +1031,7 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
   }
   if (!build_plan(p, &s.plan)) return false;
   s.zpts = (p->slab_lo || p->slab_hi) ? (int64_t)(p->slab_hi - p->slab_lo) * s.fs.k : s.fs.npt[d - 1];
+  s.nplanes = p->n_planes;
   // tables must hold the derivative levels the blocks use
   for (int k = 0; k < d; ++k)
     if (p->trial[k].max_deriv < 1) {
@@ -923,12 +1072,68 @@ bool sym_eligible(const igs_problem* p, const AsmShape& s) {
          sym_fits_for(s.fs.p, s.plan, p->n_planes, s.fs.nfn[2]);
 }
 
+// 3D three-pass path (p >= 5): pass-A row tile (TMA boxes of 16 rows), z
+// layers per G chunk (G chunk <= ~1.5 GB) and the workspace behind H and the
+// z records: [y records][G chunk][pass-A band tables].
+constexpr int A3P_YS = 16;
+struct ThreePass {
+  bool on;
+  int T;                // pass-A row tile in x
+  int64_t nzc;          // z layers per chunk
+  size_t w1_doubles, g_doubles, wg_doubles;
+};
+
+template <int P>
+int three_pass_tile(int nplanes) {
+  if (A2Cfg<P, P, 6, A3P_YS>::smem(nplanes) <= 232448) return 6;
+  if (A2Cfg<P, P, 4, A3P_YS>::smem(nplanes) <= 232448) return 4;
+  if (A2Cfg<P, P, 2, A3P_YS>::smem(nplanes) <= 232448) return 2;
+  if (A2Cfg<P, P, 1, A3P_YS>::smem(nplanes) <= 232448) return 1;
+  return 0;
+}
+
+template <int P>
+size_t three_pass_table_doubles(int T, int64_t nfn0) {
+  switch (T) {
+    case 6: return (size_t)ceil_div(nfn0, 6) * A3Cfg<P, P, 6>::W0T;
+    case 4: return (size_t)ceil_div(nfn0, 4) * A3Cfg<P, P, 4>::W0T;
+    case 2: return (size_t)ceil_div(nfn0, 2) * A3Cfg<P, P, 2>::W0T;
+    default: return (size_t)nfn0 * A3Cfg<P, P, 1>::W0T;
+  }
+}
+
+ThreePass three_pass_plan(const AsmShape& s) {
+  ThreePass t{};
+  if (s.fs.d != 3 || s.fs.p < 5) return t;
+  for (int h = 0; h < s.plan.nh; ++h)
+    if (s.plan.h_ng[h] > 4) return t;
+  if (s.plan.nh > 4) return t;
+  t.T = s.fs.p == 5 ? three_pass_tile<5>(s.nplanes) : three_pass_tile<6>(s.nplanes);
+  if (t.T == 0) return t;
+  const int W = 2 * s.fs.p - 1;
+  const size_t s0pad = (size_t)ceil_div(s.fs.nfn[0] * W, (int64_t)kSweepBlock) * kSweepBlock;
+  const size_t per_layer = s0pad * s.fs.npt[1] * s.plan.ng;  // doubles of G per z layer
+  int64_t nzc = (int64_t)(187500000 / per_layer);            // ~1.5 GB
+  if (nzc < 1) nzc = 1;
+  if (nzc > s.zpts) nzc = s.zpts;
+  t.nzc = nzc;
+  t.g_doubles = per_layer * nzc;
+  const int PP = (s.fs.p + 1) & ~1;
+  t.w1_doubles = ((size_t)s.fs.nel[1] * (s.fs.k * 4 * PP + 4) + 1) & ~size_t(1);
+  t.wg_doubles = s.fs.p == 5 ? three_pass_table_doubles<5>(t.T, s.fs.nfn[0])
+                             : three_pass_table_doubles<6>(t.T, s.fs.nfn[0]);
+  t.on = true;
+  return t;
+}
+
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
   auto padded = [](int64_t n) { return (size_t)ceil_div(n, (int64_t)kSweepBlock) * kSweepBlock; };
   if (s.fs.d == 3) {
+    const ThreePass tp = three_pass_plan(s);
+    const size_t extra = tp.on ? (tp.w1_doubles + tp.g_doubles + tp.wg_doubles + 8) * sizeof(double) : 0;
     return padded((s.fs.nfn[1] * W) * (s.fs.nfn[0] * W)) * s.zpts * s.plan.nh * sizeof(double) +
-           (size_t)s.fs.nel[2] * (s.fs.k * 4 * (s.fs.p + 1) + 4) * sizeof(double) + 512;
+           (size_t)s.fs.nel[2] * (s.fs.k * 4 * (s.fs.p + 1) + 4) * sizeof(double) + 512 + extra;
   }
   return padded(s.fs.nfn[0] * W) * s.fs.npt[1] * s.plan.ng * sizeof(double) +
          ((size_t)s.fs.nel[1] * (s.fs.k * 4 * (s.fs.p + 1) + 4) + 2) * sizeof(double) +
@@ -1017,26 +1222,170 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const ZRange
   return IGS_OK;
 }
 
+// Pass A of the three-pass path for one chunk of z layers [zc0, zc0 + nz):
+// asm2_stage1 over the chunk's rows (layer-major, y fastest).
+template <int P, int Q, int T>
+igs_status launch3_passA(const igs_problem* p, const AsmShape& s, const CUtensorMap& fmap, const double* Wg,
+                         double* G, int64_t ytma0, int64_t nz, cudaStream_t st) {
+  using C = A3Cfg<P, Q, T>;
+  Asm2Args a{};
+  a.plan = s.plan;
+  a.tab = tab_args(p);
+  a.G = G;
+  a.NS0 = s.fs.nfn[0] * C::W;
+  a.NE = nz * s.fs.nel[1];
+  a.X1 = nz * s.fs.npt[1];
+  a.ytma0 = ytma0;
+  a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
+  a.Wg = Wg;
+  const size_t smem = A2Cfg<P, Q, T, A3P_YS>::smem(p->n_planes);
+  static std::atomic<int> res_cache[17];
+  const int npl_key = p->n_planes < 0 ? 0 : (p->n_planes > 16 ? 16 : p->n_planes);
+  int resident = res_cache[npl_key].load(std::memory_order_relaxed);
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm2_stage1<P, Q, T, A3P_YS>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                     "smem attribute"));
+  if (resident <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm2_stage1<P, Q, T, A3P_YS>, A2_NT, smem) !=
+            cudaSuccess ||
+        resident < 1) {
+      cudaGetLastError();
+      resident = 1;
+    }
+    res_cache[npl_key].store(resident, std::memory_order_relaxed);
+  }
+  // rows per CTA (whole TMA boxes): minimise waves x (boxes per CTA + 2: the
+  // CTA's table copy and pipeline fill)
+  const int64_t slots = 148 * (int64_t)resident, nbox = ceil_div(a.X1, (int64_t)A3P_YS);
+  int64_t per_best = nbox;
+  {
+    int64_t best = -1;
+    for (int64_t per = 1; per <= nbox && per <= 4096; ++per) {
+      const int64_t ctas = a.nt0 * ceil_div(nbox, per);
+      const int64_t cost = ceil_div(ctas, slots) * (per + 2);
+      if (best < 0 || cost < best) {
+        best = cost;
+        per_best = per;
+      }
+    }
+  }
+  a.yc = (int)(per_best * A3P_YS);
+  const int64_t nyc = ceil_div(a.X1, (int64_t)a.yc);
+  asm2_stage1<P, Q, T, A3P_YS><<<(unsigned)(a.nt0 * nyc), A2_NT, smem, st>>>(a, fmap, p->n_planes);
+  IGS_LAUNCH_CHECK("asm2_stage1 (3D pass A)");
+  return IGS_OK;
+}
+
+template <int P, int Q, int T>
+igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const ThreePass& tp, const ZRange& z,
+                                TensorPat pat, const double* planes, double* H, double* extra,
+                                cudaStream_t st) {
+  using C = A3Cfg<P, Q, T>;
+  constexpr int W = 2 * P - 1;
+  if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
+  double* w1g = extra;
+  double* G = w1g + tp.w1_doubles;
+  double* Wg = G + tp.g_doubles;
+  const int64_t ny = s.fs.npt[1];
+  CUtensorMap fmap;
+  {
+    // rows = (layer of the held planes, y) flattened
+    const int64_t dims[4] = {s.fs.npt[0], ny * (int64_t)(z.sh - z.sl) * Q, 1, p->n_planes};
+    const unsigned box[4] = {(unsigned)C::XR, (unsigned)A3P_YS, 1u, (unsigned)p->n_planes};
+    IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
+  }
+  const TabArgs tab = tab_args(p);
+  const int nt0 = (int)ceil_div(s.fs.nfn[0], T);
+  asm2_tables_kernel<P, Q, T><<<(unsigned)nt0, 256, 0, st>>>(tab, Wg);
+  IGS_LAUNCH_CHECK("asm2_tables_kernel");
+  {
+    Asm3bArgs b{};
+    b.tab = tab;
+    b.pat = pat;
+    const int64_t n = (int64_t)tab.K[1] * S3Cfg<P, Q>::NWR;
+    asm_wlast_kernel<P, Q, 2><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(b, w1g);
+    IGS_LAUNCH_CHECK("asm_wlast_kernel (y)");
+  }
+  AsmYArgs y{};
+  y.tab = tab;
+  y.G = G;
+  y.H = H;
+  y.w1g = w1g;
+  y.NS0 = s.fs.nfn[0] * W;
+  y.NE_H = z.e_hi - z.e_lo;
+  y.ng = s.plan.ng;
+  y.nh = s.plan.nh;
+  for (int h = 0; h < 4; ++h)
+    for (int v = 0; v < 4; ++v) y.vmap[h][v] = -1;
+  for (int h = 0; h < s.plan.nh; ++h) {
+    y.h_g0[h] = s.plan.h_g0[h];
+    y.h_ng[h] = s.plan.h_ng[h];
+    for (int g = s.plan.h_g0[h]; g < s.plan.h_g0[h] + s.plan.h_ng[h]; ++g)
+      y.vmap[h][s.plan.g_v1[g]] = g - s.plan.h_g0[h];
+  }
+  constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_ysweep<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem3),
+                     "smem attribute"));
+  const int64_t z0 = (int64_t)z.e_lo * Q, z1 = (int64_t)z.e_hi * Q, zpl = (int64_t)z.sl * Q;
+  const unsigned nbs0 = (unsigned)ceil_div(y.NS0, (int64_t)kSweepBlock);
+  for (int64_t zc = z0; zc < z1; zc += tp.nzc) {
+    const int64_t nz = min64(tp.nzc, z1 - zc);
+    IGS_TRY((launch3_passA<P, Q, T>(p, s, fmap, Wg, G, (zc - zpl) * ny, nz, st)));
+    y.NE_G = nz * s.fs.nel[1];
+    y.zrel0 = zc - z0;
+    dim3 grid(nbs0, (unsigned)nz, (unsigned)s.plan.nh);
+    asm_ysweep<P, Q><<<grid, NT3, smem3, st>>>(y);
+    IGS_LAUNCH_CHECK("asm_ysweep");
+  }
+  return IGS_OK;
+}
+
+template <int P, int Q>
+igs_status launch3_three_pass(const igs_problem* p, const AsmShape& s, const ThreePass& tp, const ZRange& z,
+                              TensorPat pat, const double* planes, double* H, double* extra, cudaStream_t st) {
+  if constexpr (P >= 5) {
+    switch (tp.T) {
+      case 6: return launch3_three_pass_T<P, Q, 6>(p, s, tp, z, pat, planes, H, extra, st);
+      case 4: return launch3_three_pass_T<P, Q, 4>(p, s, tp, z, pat, planes, H, extra, st);
+      case 2: return launch3_three_pass_T<P, Q, 2>(p, s, tp, z, pat, planes, H, extra, st);
+      case 1: return launch3_three_pass_T<P, Q, 1>(p, s, tp, z, pat, planes, H, extra, st);
+      default: break;
+    }
+  }
+  return fail(IGS_ECAPACITY, "no three-pass assembly for this order");
+}
+
 template <int P, int Q>
 igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
                    const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st,
-                   bool kernel_only) {
+                   bool kernel_only, bool two_pass) {
   if (row_hi <= row_lo) return IGS_OK;
   ZRange z;
   IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
   const int tile = asm3_tile<P>(s.plan, p->n_planes);
   if (tile == 0) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
-  if constexpr (kWideTile<P> > 0) {
-    if (tile == kWideTile<P>) IGS_TRY((launch3_stage12<P, Q, kWideTile<P>>(p, s, z, planes, H, st)));
-  }
-  if (tile == 4) IGS_TRY((launch3_stage12<P, Q, 4>(p, s, z, planes, H, st)));
-  else if (tile == 2) IGS_TRY((launch3_stage12<P, Q, 2>(p, s, z, planes, H, st)));
-  else if (tile == 1) IGS_TRY((launch3_stage12<P, Q, 1>(p, s, z, planes, H, st)));
-  if (kernel_only) return IGS_OK;  // measurement: the dominant kernel alone
   constexpr int W = 2 * P - 1;
   struct {
     int64_t NS0, NS1;
   } a{s.fs.nfn[0] * W, s.fs.nfn[1] * W};
+  // p >= 5: x and y contractions as separate passes (G chunks through HBM)
+  // unless IGS_FLAG_TWO_PASS asks for the fused stage-1/2 kernel
+  const ThreePass tp = three_pass_plan(s);
+  if (tp.on && tile < 4 && !two_pass) {
+    const int64_t nbh = ceil_div(a.NS0 * a.NS1, (int64_t)kSweepBlock);
+    double* extra = H + (size_t)nbh * kSweepBlock * (z.sh - z.sl) * Q * s.plan.nh +
+                    (size_t)s.fs.nel[2] * (Q * 4 * (P + 1) + 4);
+    IGS_TRY((launch3_three_pass<P, Q>(p, s, tp, z, pat, planes, H, extra, st)));
+  } else {
+    if constexpr (kWideTile<P> > 0) {
+      if (tile == kWideTile<P>) IGS_TRY((launch3_stage12<P, Q, kWideTile<P>>(p, s, z, planes, H, st)));
+    }
+    if (tile == 4) IGS_TRY((launch3_stage12<P, Q, 4>(p, s, z, planes, H, st)));
+    else if (tile == 2) IGS_TRY((launch3_stage12<P, Q, 2>(p, s, z, planes, H, st)));
+    else if (tile == 1) IGS_TRY((launch3_stage12<P, Q, 1>(p, s, z, planes, H, st)));
+  }
+  if (kernel_only) return IGS_OK;  // measurement: the dominant kernel alone
   const TabArgs tab = tab_args(p);
   Asm3bArgs b{};
   b.plan = s.plan;
@@ -1084,6 +1433,8 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
   a.G = G;
   a.NS0 = s.fs.nfn[0] * C::W;
   a.NE = s.fs.nel[1];
+  a.X1 = s.fs.npt[1];
+  a.ytma0 = 0;
   a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
   const size_t smem = A2Cfg<P, Q, T>::smem(p->n_planes);
   if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
@@ -1309,7 +1660,8 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
   bool done = false;
 #define IGS_ASM_CASE(PP, QQ)                                                                    \
   if (!done && P == PP && Q == QQ) {                                                            \
-    r = p->d == 3 ? launch3<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko)   \
+    r = p->d == 3 ? launch3<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko,   \
+                                     (flags & IGS_FLAG_TWO_PASS) != 0)                            \
                   : launch2<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko);  \
     done = true;                                                                                \
   }
