@@ -598,8 +598,9 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       const double* hcol = hst + stg * C::HST + tid;
       const double* wst = w2s + stg * NWR;
       // Σ_{θ,η} (wB^θ_jn)(B^η_jm) H_{θ+2η}: contract θ first (u_η[jn]),
-      // then η into the ring (P·P·2 + 4P FMAs, 4P broadcast factors per q)
-#pragma unroll
+      // then η into the ring (P·P·2 + 4P FMAs, 4P broadcast factors per q);
+      // p >= 5 keeps the point loop rolled (instruction-cache footprint)
+#pragma unroll(P >= 5 ? 1 : Q)
       for (int q = 0; q < Q; ++q) {
         double hv[4];
 #pragma unroll
@@ -680,15 +681,29 @@ struct AsmYArgs {
   int vmap[4][4];       // [h][v1]: group (relative to h_g0[h]) holding y variant v1, -1: none
 };
 
+// Pipeline of the y sweep: NSY element stages, NSY - 1 elements ahead (the
+// per-stage tiles are small — Q bulk copies of hng·1 KB — so the copy
+// latency, not the DRAM stream count, is what the ring has to cover).
+constexpr int NSY = 2, DY = NSY - 1;
 template <int P, int Q>
-__global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs a) {
+struct SYCfg {
   using C = S3Cfg<P, Q>;
-  constexpr int W = 2 * P - 1, NWT = C::NWT, NWR = C::NWR, PP = C::PP;
-  extern __shared__ __align__(16) double s3[];
-  double* hst = s3;                    // [NS3][Q][hng][NT3]
-  double* w2s = s3 + NS3 * C::HST;     // [NS3][NWR]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWR);
+  static constexpr size_t SMEM = (size_t)NSY * (C::HST + C::NWR) * sizeof(double) + NSY * sizeof(uint64_t);
+};
+
+// TH / ET: the stage-2 group has y variants with a trial (θ) / test (η)
+// derivative; absent ones are compiled out (u_η = Σ_θ (wB^θ) G_{θ+2η},
+// ring += Σ_η B^η u_η).
+template <int P, int Q, bool TH, bool ET>
+__device__ __forceinline__ void ysweep_body(const AsmYArgs& a, double* s3) {
+  using C = S3Cfg<P, Q>;
+  constexpr int W = 2 * P - 1, NWR = C::NWR, PP = C::PP;
+  double* hst = s3;                    // [NSY][Q][hng][NT3]
+  double* w2s = s3 + NSY * C::HST;     // [NSY][NWR]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NSY * NWR);
   const int tid = threadIdx.x;
+  // h is the slowest grid index: co-resident CTAs then run the same
+  // specialisation (h fastest measured 2x slower: instruction-cache misses)
   const int64_t sb = blockIdx.x;
   const int zl = blockIdx.y, h = blockIdx.z;
   const int hng = a.h_ng[h], g0 = a.h_g0[h];
@@ -707,11 +722,22 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs
 #pragma unroll
     for (int k = 0; k < W; ++k) ring[r][k] = 0.0;
   // row m1 is final: its 2P-1 slots s1 = m1·W + k of this thread's s0
+  // sweep_offset(sp) = (sp / 128)·S + c + sp % 128 with S = NE·Q·nh·128 and
+  // c = ((ez·Q + qz)·nh + h)·128; consecutive slots advance sp by NS0
+  const int64_t hS = a.NE_H * Q * a.nh * kSweepBlock;
+  double* const hc = a.H + ((ez * Q + qz) * a.nh + h) * kSweepBlock;
+  const int ns_blk = (int)(a.NS0 / kSweepBlock), ns_rem = (int)(a.NS0 % kSweepBlock);
   auto flush = [&](int64_t m1, const double* row) {
+    const int64_t sp0 = (m1 * W) * a.NS0 + s0;
+    int64_t blk = sp0 / kSweepBlock;
+    int lo = (int)(sp0 % kSweepBlock);
 #pragma unroll
     for (int k = 0; k < W; ++k) {
-      const int64_t sp = (m1 * W + k) * a.NS0 + s0;
-      a.H[sweep_offset(sp, ez, qz, h, a.NE_H, Q, a.nh)] = row[k];
+      hc[blk * hS + lo] = row[k];
+      lo += ns_rem;
+      const int carry = lo >= kSweepBlock ? 1 : 0;
+      lo -= carry * kSweepBlock;
+      blk += ns_blk + carry;
     }
   };
   const unsigned qbytes = (unsigned)(hng * NT3 * sizeof(double));
@@ -719,7 +745,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs
   const double* gblock = a.G + ((sb * a.NE_G + (int64_t)zl * K1) * Q * a.ng + g0) * NT3;
   auto issue = [&](int e1) {  // one thread
     if (e1 >= K1) return;
-    const int stg = e1 % NS3;
+    const int stg = e1 % NSY;
     dev::mbar_expect_tx(bars + stg, Q * qbytes + wbytes);
 #pragma unroll
     for (int q = 0; q < Q; ++q)
@@ -727,33 +753,39 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs
                      bars + stg);
     dev::bulk_load(w2s + stg * NWR, a.w1g + (int64_t)e1 * NWR, wbytes, bars + stg);
   };
-  if (tid < NS3) dev::mbar_init(bars + tid, 1);
+  if (tid < NSY) dev::mbar_init(bars + tid, 1);
   dev::fence_mbar_init();
   __syncthreads();
   if (tid == 0)
-    for (int e = 0; e < D3; ++e) issue(e);
+    for (int e = 0; e < DY; ++e) issue(e);
   for (int eb = 0; eb < K1; eb += P) {
 #pragma unroll
     for (int r = 0; r < P; ++r) {  // ring row of element e1 is static: r
       const int e1 = eb + r;
       if (e1 >= K1) break;
-      __syncthreads();  // stage (e1 + D3) % NS3 was last read for element e1 - 1
+      __syncthreads();  // stage (e1 + DY) % NSY was last read for element e1 - 1
       if (tid == 0) {
         dev::fence_proxy_async();
-        issue(e1 + D3);
+        issue(e1 + DY);
       }
-      const int stg = e1 % NS3;
-      dev::mbar_wait(bars + stg, (unsigned)((e1 / NS3) & 1));
+      const int stg = e1 % NSY;
+      dev::mbar_wait(bars + stg, (unsigned)((e1 / NSY) & 1));
       const double* hcol = hst + stg * C::HST + tid;
       const double* wst = w2s + stg * NWR;
-#pragma unroll
+      // (the point loop stays rolled: P·Q unrolled copies of the update
+      // overflow the instruction cache — `no_inst` was the top stall)
+#pragma unroll 1
       for (int q = 0; q < Q; ++q) {
         double hv[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) hv[v] = vm[v] >= 0 ? hcol[(q * hng + vm[v]) * NT3] : 0.0;
+        for (int v = 0; v < 4; ++v) {
+          const bool used = (TH || !(v & 1)) && (ET || !(v & 2));
+          hv[v] = used && vm[v] >= 0 ? hcol[(q * hng + vm[v]) * NT3] : 0.0;
+        }
         double fb[4][P];
 #pragma unroll
-        for (int f = 0; f < 4; ++f)
+        for (int f = 0; f < 4; ++f) {
+          if ((f == 1 && !TH) || (f == 3 && !ET)) continue;
 #pragma unroll
           for (int j = 0; j < P; j += 2) {
             if (j + 1 < P) {
@@ -764,18 +796,20 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs
               fb[f][j] = wst[(q * 4 + f) * PP + j];
             }
           }
+        }
         double u0[P], u1[P];
 #pragma unroll
         for (int jn = 0; jn < P; ++jn) {
-          u0[jn] = fma(fb[1][jn], hv[1], fb[0][jn] * hv[0]);
-          u1[jn] = fma(fb[1][jn], hv[3], fb[0][jn] * hv[2]);
+          u0[jn] = TH ? fma(fb[1][jn], hv[1], fb[0][jn] * hv[0]) : fb[0][jn] * hv[0];
+          if (ET) u1[jn] = TH ? fma(fb[1][jn], hv[3], fb[0][jn] * hv[2]) : fb[0][jn] * hv[2];
         }
 #pragma unroll
         for (int jm = 0; jm < P; ++jm)
 #pragma unroll
           for (int jn = 0; jn < P; ++jn) {
             double& acc = ring[(r + jm) % P][jn - jm + P - 1];
-            acc = fma(fb[3][jm], u1[jn], fma(fb[2][jm], u0[jn], acc));
+            if (ET) acc = fma(fb[3][jm], u1[jn], fma(fb[2][jm], u0[jn], acc));
+            else acc = fma(fb[2][jm], u0[jn], acc);
           }
       }
       if (valid) flush(e1, ring[r]);
@@ -794,6 +828,18 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 2) asm_ysweep(const AsmYArgs
         if (s == slot) flush(m1, ring[s]);
     }
   }
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(NT3, 2) asm_ysweep(const AsmYArgs a) {
+  extern __shared__ __align__(16) double s3y[];
+  const int h = blockIdx.z;
+  const bool th = a.vmap[h][1] >= 0 || a.vmap[h][3] >= 0;
+  const bool et = a.vmap[h][2] >= 0 || a.vmap[h][3] >= 0;
+  if (th && et) ysweep_body<P, Q, true, true>(a, s3y);
+  else if (th) ysweep_body<P, Q, true, false>(a, s3y);
+  else if (et) ysweep_body<P, Q, false, true>(a, s3y);
+  else ysweep_body<P, Q, false, false>(a, s3y);
 }
 
 // ---------------------------------------------------------------- 2D -------
@@ -1323,7 +1369,7 @@ igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const T
     for (int g = s.plan.h_g0[h]; g < s.plan.h_g0[h] + s.plan.h_ng[h]; ++g)
       y.vmap[h][s.plan.g_v1[g]] = g - s.plan.h_g0[h];
   }
-  constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
+  constexpr size_t smem3 = SYCfg<P, Q>::SMEM;
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_ysweep<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem3),
                      "smem attribute"));

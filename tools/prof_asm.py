@@ -9,7 +9,11 @@ sys.path.insert(0, ".")
 from paper_1809_05471_b200 import sumfac, workloads  # noqa: E402
 
 name = sys.argv[1]
-c = workloads.CONFIGS[name]
+if "," in name:  # "d,p,K,kind"
+    d_, p_, K_, kind_ = (int(v) for v in name.split(","))
+    c = {"d": d_, "p": p_, "K": K_, "kind": kind_}
+else:
+    c = workloads.CONFIGS[name]
 prob = workloads.make_problem(c["d"], c["p"], c["K"], c["kind"])
 A = sumfac.assemble(prob)
 torch.cuda.synchronize()
