@@ -971,6 +971,121 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
   }
 }
 
+// Pass A kernel of the three-pass path: asm2_stage1's banded GEMM with
+//   * TMA boxes of 16 rows (the 7-plane regions of p = 5, 6 then fit twice),
+//     row pitch XB ≡ 4 or 12 (mod 16) doubles so the A-fragment loads (8
+//     rows x 4 columns) are bank-conflict-free (the plain region width 54 /
+//     50 gave 35 % conflict wavefronts);
+//   * one warp per (y tile, slot tile, half of the blocks — whole groups), so
+//     every warp has a task in every stage (12-14 tasks on 16 warps left a
+//     quarter of the CTA idle at the stage barrier).
+template <int P, int Q, int T>
+struct AXCfg {
+  using B = A3Cfg<P, Q, T>;
+  static constexpr int YS = 16;
+  static constexpr int xb() {
+    int b = B::XK;  // >= the region width, covers the k-step tail
+    while (b % 16 != 4 && b % 16 != 12) b += 2;
+    return b;
+  }
+  static constexpr int XB = xb();
+  static constexpr int NTASK = (YS / 8) * (B::PTP / 8) * 2;
+  static constexpr int NW = NTASK < 32 ? NTASK : 32;
+  static constexpr int NT = NW * 32;
+  static constexpr size_t fbox(int npl) { return ((size_t)npl * YS * XB + 4 + 15) & ~size_t(15); }
+  static constexpr size_t smem(int npl) { return (2 * fbox(npl) + B::W0T) * sizeof(double) + 32; }
+  static_assert(XB <= 256 && XB >= B::XK, "TMA box / k-step tail");
+};
+
+template <int P, int Q, int T>
+__global__ void __launch_bounds__(AXCfg<P, Q, T>::NT) asm3_xpass(const Asm2Args a,
+                                                                  const __grid_constant__ CUtensorMap fmap,
+                                                                  int nplanes) {
+  using C = A3Cfg<P, Q, T>;
+  using CX = AXCfg<P, Q, T>;
+  constexpr int PT = C::PT, PTP = C::PTP, XK = C::XK, SP = C::SP, W = C::W, SR = C::SR;
+  constexpr int YS = CX::YS, XB = CX::XB, NT = CX::NT, NW = CX::NW;
+  constexpr int KL = max_ksteps<P, Q, T>(PTP / 8, XK / 4);
+  constexpr int NST = PTP / 8;
+  extern __shared__ __align__(128) double sm[];
+  const AsmPlan& pl = a.plan;
+  const size_t fb = CX::fbox(nplanes);
+  double* Fs = sm;                 // [2][nplanes][YS][XB]
+  double* W0 = Fs + 2 * fb;        // [4][XK][SP]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(W0 + C::W0T);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, m4 = lane & 3;
+  const int a0 = (blockIdx.x % a.nt0) * T;
+  const int xb0 = (a0 - (P - 1)) * Q;
+  const int64_t X1 = a.X1;
+  const int64_t y_lo = (int64_t)(blockIdx.x / a.nt0) * a.yc;
+  const int64_t y_hi = min64(X1, y_lo + a.yc);
+  const int nstage = (int)((y_hi - y_lo + YS - 1) / YS);
+  const unsigned fbytes = (unsigned)((size_t)nplanes * YS * XB * sizeof(double));
+  for (int b = 0; b < 2; ++b)
+    for (size_t i = (size_t)nplanes * YS * XB + tid; i < fb; i += NT) Fs[b * fb + i] = 0.0;
+  if (tid < 3) dev::mbar_init(bar + tid, 1);
+  dev::fence_mbar_init();
+  dev::fence_proxy_async();
+  __syncthreads();
+  if (tid == 0) {
+    constexpr unsigned wbytes = (unsigned)(C::W0T * sizeof(double));
+    dev::mbar_expect_tx(bar + 2, wbytes);
+    dev::bulk_load(W0, a.Wg + (size_t)(blockIdx.x % a.nt0) * C::W0T, wbytes, bar + 2);
+    for (int i = 0; i < 2 && i < nstage; ++i) {
+      dev::mbar_expect_tx(bar + i, fbytes);
+      dev::tma_load_4d(Fs + i * fb, &fmap, bar + i, xb0, (int)(a.ytma0 + y_lo + i * YS), 0, 0);
+    }
+  }
+  dev::mbar_wait(bar + 2, 0u);
+  for (int i = 0; i < nstage; ++i) {
+    const int buf = i & 1;
+    dev::mbar_wait(bar + buf, (unsigned)((i >> 1) & 1));
+    const double* Fb0 = Fs + buf * fb;
+    const int64_t y0 = y_lo + (int64_t)i * YS;
+    for (int t = warp; t < CX::NTASK; t += NW) {
+      const int half = t & 1, yb = (t >> 1) / NST, st = (t >> 1) % NST;
+      int k_lo, k_hi;
+      slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
+      const double* Fy = Fb0 + (yb * 8 + g8) * XB + m4 + k_lo * 4;
+      const double* Wk = W0 + (m4 + k_lo * 4) * SP + st * 8 + g8;
+      const int64_t y = y0 + yb * 8 + g8;
+      const int s = st * 8 + 2 * m4;
+      const int64_t gs0 = (int64_t)(a0 + s / SR) * W + s % SR;
+      const int64_t gs0b = (int64_t)(a0 + (s + 1) / SR) * W + (s + 1) % SR;
+      const bool ok0 = y < y_hi && s < PT && s % SR < W && gs0 < a.NS0;
+      const bool ok1 = y < y_hi && s + 1 < PT && (s + 1) % SR < W && gs0b < a.NS0;
+      // G offsets of group 0 (sweep-blocked): groups advance by 128 doubles
+      const int64_t off0 = sweep_offset(gs0, y / Q, (int)(y % Q), 0, a.NE, Q, pl.ng);
+      const int64_t off1 = sweep_offset(gs0b, y / Q, (int)(y % Q), 0, a.NE, Q, pl.ng);
+      const int b_lo = half ? pl.half_b : 0, b_hi = half ? pl.nb : pl.half_b;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < kMaxBlocks; ++b) {
+        if (b < b_lo) continue;
+        if (b >= b_hi) break;
+        const double* Fb = Fy + pl.b_plane[b] * (YS * XB);
+        const double* Wb = Wk + pl.b_v0[b] * (XK * SP);
+#pragma unroll
+        for (int kk = 0; kk < KL; ++kk)
+          if (k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
+        if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
+          const int hoff = pl.b_g[b] * kSweepBlock;
+          if (ok0) a.G[off0 + hoff] = d0;
+          if (ok1) a.G[off1 + hoff] = d1;
+          d0 = d1 = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && i + 2 < nstage) {
+      dev::fence_proxy_async();
+      dev::mbar_expect_tx(bar + buf, fbytes);
+      dev::tma_load_4d(Fs + buf * fb, &fmap, bar + buf, xb0, (int)(a.ytma0 + y0 + 2 * YS), 0, 0);
+    }
+  }
+}
+
 // ---- host side ----------------------------------------------------------------
 
 // Row tile per direction of the 3D stage-1/2 kernel: the largest of 4, 2, 1
@@ -1131,10 +1246,10 @@ struct ThreePass {
 
 template <int P>
 int three_pass_tile(int nplanes) {
-  if (A2Cfg<P, P, 6, A3P_YS>::smem(nplanes) <= 232448) return 6;
-  if (A2Cfg<P, P, 4, A3P_YS>::smem(nplanes) <= 232448) return 4;
-  if (A2Cfg<P, P, 2, A3P_YS>::smem(nplanes) <= 232448) return 2;
-  if (A2Cfg<P, P, 1, A3P_YS>::smem(nplanes) <= 232448) return 1;
+  if (AXCfg<P, P, 6>::smem(nplanes) <= 232448) return 6;
+  if (AXCfg<P, P, 4>::smem(nplanes) <= 232448) return 4;
+  if (AXCfg<P, P, 2>::smem(nplanes) <= 232448) return 2;
+  if (AXCfg<P, P, 1>::smem(nplanes) <= 232448) return 1;
   return 0;
 }
 
@@ -1284,15 +1399,16 @@ igs_status launch3_passA(const igs_problem* p, const AsmShape& s, const CUtensor
   a.ytma0 = ytma0;
   a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
   a.Wg = Wg;
-  const size_t smem = A2Cfg<P, Q, T, A3P_YS>::smem(p->n_planes);
+  using CX = AXCfg<P, Q, T>;
+  const size_t smem = CX::smem(p->n_planes);
   static std::atomic<int> res_cache[17];
   const int npl_key = p->n_planes < 0 ? 0 : (p->n_planes > 16 ? 16 : p->n_planes);
   int resident = res_cache[npl_key].load(std::memory_order_relaxed);
-  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm2_stage1<P, Q, T, A3P_YS>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_xpass<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem),
                      "smem attribute"));
   if (resident <= 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm2_stage1<P, Q, T, A3P_YS>, A2_NT, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm3_xpass<P, Q, T>, CX::NT, smem) !=
             cudaSuccess ||
         resident < 1) {
       cudaGetLastError();
@@ -1317,8 +1433,8 @@ igs_status launch3_passA(const igs_problem* p, const AsmShape& s, const CUtensor
   }
   a.yc = (int)(per_best * A3P_YS);
   const int64_t nyc = ceil_div(a.X1, (int64_t)a.yc);
-  asm2_stage1<P, Q, T, A3P_YS><<<(unsigned)(a.nt0 * nyc), A2_NT, smem, st>>>(a, fmap, p->n_planes);
-  IGS_LAUNCH_CHECK("asm2_stage1 (3D pass A)");
+  asm3_xpass<P, Q, T><<<(unsigned)(a.nt0 * nyc), CX::NT, smem, st>>>(a, fmap, p->n_planes);
+  IGS_LAUNCH_CHECK("asm3_xpass");
   return IGS_OK;
 }
 
@@ -1337,7 +1453,7 @@ igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const T
   {
     // rows = (layer of the held planes, y) flattened
     const int64_t dims[4] = {s.fs.npt[0], ny * (int64_t)(z.sh - z.sl) * Q, 1, p->n_planes};
-    const unsigned box[4] = {(unsigned)C::XR, (unsigned)A3P_YS, 1u, (unsigned)p->n_planes};
+    const unsigned box[4] = {(unsigned)AXCfg<P, Q, T>::XB, (unsigned)A3P_YS, 1u, (unsigned)p->n_planes};
     IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
   }
   const TabArgs tab = tab_args(p);
