@@ -976,9 +976,10 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
 //     row pitch XB ≡ 4 or 12 (mod 16) doubles so the A-fragment loads (8
 //     rows x 4 columns) are bank-conflict-free (the plain region width 54 /
 //     50 gave 35 % conflict wavefronts);
-//   * one warp per (y tile, slot tile, half of the blocks — whole groups), so
-//     every warp has a task in every stage (12-14 tasks on 16 warps left a
-//     quarter of the CTA idle at the stage barrier).
+//   * one warp per (slot tile, half of the blocks — whole groups) for both y
+//     tiles of the box: every warp has a task in every stage (12-14 tasks on
+//     16 warps left a quarter of the CTA idle at the stage barrier) and each
+//     W fragment feeds two DMMAs (3 fragment loads per 2 MMAs).
 template <int P, int Q, int T>
 struct AXCfg {
   using B = A3Cfg<P, Q, T>;
@@ -989,7 +990,7 @@ struct AXCfg {
     return b;
   }
   static constexpr int XB = xb();
-  static constexpr int NTASK = (YS / 8) * (B::PTP / 8) * 2;
+  static constexpr int NTASK = (B::PTP / 8) * 2;  // (slot tile, half of the blocks), both y tiles
   static constexpr int NW = NTASK < 32 ? NTASK : 32;
   static constexpr int NT = NW * 32;
   static constexpr size_t fbox(int npl) { return ((size_t)npl * YS * XB + 4 + 15) & ~size_t(15); }
@@ -1044,22 +1045,28 @@ __global__ void __launch_bounds__(AXCfg<P, Q, T>::NT) asm3_xpass(const Asm2Args 
     const double* Fb0 = Fs + buf * fb;
     const int64_t y0 = y_lo + (int64_t)i * YS;
     for (int t = warp; t < CX::NTASK; t += NW) {
-      const int half = t & 1, yb = (t >> 1) / NST, st = (t >> 1) % NST;
+      const int half = t & 1, st = t >> 1;
       int k_lo, k_hi;
       slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
-      const double* Fy = Fb0 + (yb * 8 + g8) * XB + m4 + k_lo * 4;
+      const double* Fy = Fb0 + g8 * XB + m4 + k_lo * 4;  // y tile 0; tile 1 at + 8·XB
       const double* Wk = W0 + (m4 + k_lo * 4) * SP + st * 8 + g8;
-      const int64_t y = y0 + yb * 8 + g8;
       const int s = st * 8 + 2 * m4;
       const int64_t gs0 = (int64_t)(a0 + s / SR) * W + s % SR;
       const int64_t gs0b = (int64_t)(a0 + (s + 1) / SR) * W + (s + 1) % SR;
-      const bool ok0 = y < y_hi && s < PT && s % SR < W && gs0 < a.NS0;
-      const bool ok1 = y < y_hi && s + 1 < PT && (s + 1) % SR < W && gs0b < a.NS0;
-      // G offsets of group 0 (sweep-blocked): groups advance by 128 doubles
-      const int64_t off0 = sweep_offset(gs0, y / Q, (int)(y % Q), 0, a.NE, Q, pl.ng);
-      const int64_t off1 = sweep_offset(gs0b, y / Q, (int)(y % Q), 0, a.NE, Q, pl.ng);
+      const bool sok0 = s < PT && s % SR < W && gs0 < a.NS0;
+      const bool sok1 = s + 1 < PT && (s + 1) % SR < W && gs0b < a.NS0;
+      // G offsets of group 0 (sweep-blocked; groups advance by 128 doubles), per y tile
+      int64_t off0[2], off1[2];
+      bool yok[2];
+#pragma unroll
+      for (int jy = 0; jy < 2; ++jy) {
+        const int64_t y = y0 + jy * 8 + g8;
+        yok[jy] = y < y_hi;
+        off0[jy] = sweep_offset(gs0, y / Q, (int)(y % Q), 0, a.NE, Q, pl.ng);
+        off1[jy] = sweep_offset(gs0b, y / Q, (int)(y % Q), 0, a.NE, Q, pl.ng);
+      }
       const int b_lo = half ? pl.half_b : 0, b_hi = half ? pl.nb : pl.half_b;
-      double d0 = 0.0, d1 = 0.0;
+      double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
 #pragma unroll
       for (int b = 0; b < kMaxBlocks; ++b) {
         if (b < b_lo) continue;
@@ -1068,12 +1075,18 @@ __global__ void __launch_bounds__(AXCfg<P, Q, T>::NT) asm3_xpass(const Asm2Args 
         const double* Wb = Wk + pl.b_v0[b] * (XK * SP);
 #pragma unroll
         for (int kk = 0; kk < KL; ++kk)
-          if (k_lo + kk < k_hi) dmma_a(d0, d1, Fb[kk * 4], Wb[kk * 4 * SP]);
+          if (k_lo + kk < k_hi) {
+            const double w = Wb[kk * 4 * SP];
+            dmma_a(c0[0], c0[1], Fb[kk * 4], w);
+            dmma_a(c1[0], c1[1], Fb[kk * 4 + 8 * XB], w);
+          }
         if (b + 1 == pl.nb || pl.b_g[b + 1] != pl.b_g[b]) {
           const int hoff = pl.b_g[b] * kSweepBlock;
-          if (ok0) a.G[off0 + hoff] = d0;
-          if (ok1) a.G[off1 + hoff] = d1;
-          d0 = d1 = 0.0;
+          if (sok0 && yok[0]) a.G[off0[0] + hoff] = c0[0];
+          if (sok1 && yok[0]) a.G[off1[0] + hoff] = c0[1];
+          if (sok0 && yok[1]) a.G[off0[1] + hoff] = c1[0];
+          if (sok1 && yok[1]) a.G[off1[1] + hoff] = c1[1];
+          c0[0] = c0[1] = c1[0] = c1[1] = 0.0;
         }
       }
     }
