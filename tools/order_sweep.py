@@ -11,6 +11,19 @@ sys.path.insert(0, ".")
 from paper_1809_05471_b200 import matfree, sumfac, workloads  # noqa: E402
 
 BW = 6544.3e9
+P64 = 37.14e12  # sustained DMMA peak, profiles/fp64_peak.json
+
+
+def _ref_frac(prob, A, ms):
+    """Reference-equivalent roofline fraction of an assembly:
+    max(F_ref / (t·P64), B_alg / (t·BW)) with F_ref = 2 x the reference
+    FlopCounter's block-update MACs and B_alg = planes read + values written."""
+    c = sumfac.FlopCounter()
+    sumfac.assemble(prob, counter=c)
+    t = ms / 1e3
+    f_ref = 2.0 * c.block_update
+    b_alg = 8.0 * prob.coeff.n_planes * prob.quad.num_points + 8.0 * A.nnz
+    return f_ref, max(f_ref / t / P64, b_alg / t / BW)
 
 
 def apply_row(p, kind, K=128, reps=10):
@@ -47,8 +60,9 @@ def asm_row(p, kind, K=64, reps=5):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    f_ref, frac = _ref_frac(prob, A, ms)
     print(f"assemble p={p} kind={'K' if kind == 2 else 'M+K'} 64^3: {ms:8.3f} ms  {A.nnz / ms / 1e6:6.2f} G nnz/s  "
-          f"nnz {A.nnz}  fused={sumfac.fused_path(prob)}", flush=True)
+          f"nnz {A.nnz}  F_ref {f_ref / 1e9:7.2f} GFLOP  frac_ref {frac:.3f}  fused={sumfac.fused_path(prob)}", flush=True)
     del prob, A
     torch.cuda.empty_cache()
 
@@ -64,8 +78,9 @@ def asm2_row(p, kind, K=256, reps=10):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    f_ref, frac = _ref_frac(prob, A, ms)
     print(f"assemble2d p={p} kind={'K' if kind == 2 else 'M+K'} 256^2: {ms:8.3f} ms  {A.nnz / ms / 1e6:6.2f} G nnz/s  "
-          f"nnz {A.nnz}  fused={sumfac.fused_path(prob)}", flush=True)
+          f"nnz {A.nnz}  F_ref {f_ref / 1e9:7.2f} GFLOP  frac_ref {frac:.3f}  fused={sumfac.fused_path(prob)}", flush=True)
     del prob, A
     torch.cuda.empty_cache()
 
