@@ -107,8 +107,10 @@ enum {
                                    values untouched; the one-pass symmetric assembly is a
                                    single kernel and runs whole) — the roofline's
                                    dominant kernel                                       */
-  IGS_FLAG_TWO_PASS = 8,        /* assembly: the two-kernel fused path (intermediate H in
-                                   HBM) even where the one-pass symmetric kernel applies */
+  IGS_FLAG_TWO_PASS = 8,        /* assembly: the two-kernel fused path (stage-1/2 kernel,
+                                   intermediate H in HBM) even where the one-pass
+                                   symmetric kernel (3D p = 2, 4; 2D) or the three-pass
+                                   path (3D p = 5, 6) applies                            */
   IGS_FLAG_SPLIT_BOUNDARY = 16  /* igs_apply_sharded: interior / boundary launches even
                                    without a next rank (exercises the overlap path)     */
 };
