@@ -1111,11 +1111,13 @@ int asm3_tile(const AsmPlan& pl, int nplanes) {
   // low orders: wider tiles so both stages have >= 16 warp tasks (and, for
   // p = 3, a region of whole MMA row tiles); else the largest of 4, 2, 1
   constexpr int wide = kWideTile<P>;
+  // (the TMA box is XR points wide: its rows must be 16-byte multiples, which
+  // rules out 1-row tiles at odd p)
   if constexpr (wide > 0)
-    if (A3Cfg<P, P, wide>::smem(nplanes, pl.ng) <= 232448) return wide;
-  if (A3Cfg<P, P, 4>::smem(nplanes, pl.ng) <= 232448) return 4;
-  if (A3Cfg<P, P, 2>::smem(nplanes, pl.ng) <= 232448) return 2;
-  if (A3Cfg<P, P, 1>::smem(nplanes, pl.ng) <= 232448) return 1;
+    if (A3Cfg<P, P, wide>::smem(nplanes, pl.ng) <= 232448 && A3Cfg<P, P, wide>::XR % 2 == 0) return wide;
+  if (A3Cfg<P, P, 4>::smem(nplanes, pl.ng) <= 232448 && A3Cfg<P, P, 4>::XR % 2 == 0) return 4;
+  if (A3Cfg<P, P, 2>::smem(nplanes, pl.ng) <= 232448 && A3Cfg<P, P, 2>::XR % 2 == 0) return 2;
+  if (A3Cfg<P, P, 1>::smem(nplanes, pl.ng) <= 232448 && A3Cfg<P, P, 1>::XR % 2 == 0) return 1;
   return 0;
 }
 
@@ -1133,10 +1135,11 @@ int asm3_tile_for(int P, const AsmPlan& pl, int nplanes) {
 // row tile of the 2D stage-1 kernel: the largest of 8, 4, 2, 1 that fits
 template <int P>
 int asm2_tile(int nplanes) {
-  if (A2Cfg<P, P, 8>::smem(nplanes) <= 232448) return 8;
-  if (A2Cfg<P, P, 4>::smem(nplanes) <= 232448) return 4;
-  if (A2Cfg<P, P, 2>::smem(nplanes) <= 232448) return 2;
-  if (A2Cfg<P, P, 1>::smem(nplanes) <= 232448) return 1;
+  // (TMA box rows of XR points must be 16-byte multiples)
+  if (A2Cfg<P, P, 8>::smem(nplanes) <= 232448 && A3Cfg<P, P, 8>::XR % 2 == 0) return 8;
+  if (A2Cfg<P, P, 4>::smem(nplanes) <= 232448 && A3Cfg<P, P, 4>::XR % 2 == 0) return 4;
+  if (A2Cfg<P, P, 2>::smem(nplanes) <= 232448 && A3Cfg<P, P, 2>::XR % 2 == 0) return 2;
+  if (A2Cfg<P, P, 1>::smem(nplanes) <= 232448 && A3Cfg<P, P, 1>::XR % 2 == 0) return 1;
   return 0;
 }
 
@@ -1182,6 +1185,8 @@ struct AsmShape {
   int nplanes;
 };
 
+bool three_pass_available(const AsmShape& s);
+
 bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
   AsmShape s;
   if (p->d != 2 && p->d != 3) return false;
@@ -1213,7 +1218,8 @@ bool asm_shape(const igs_problem* p, const Dims& D, AsmShape* out) {
         if (s.plan.b_v0[b] != 0) return false;
     }
   if (s.fs.p < 2 || s.fs.p > 6 || s.fs.k != s.fs.p) return false;
-  if (d == 3 && asm3_tile_for(s.fs.p, s.plan, p->n_planes) == 0) return false;  // stage-1/2 tile must fit
+  // a stage-1/2 tile must fit, or the three-pass path serves the order
+  if (d == 3 && asm3_tile_for(s.fs.p, s.plan, p->n_planes) == 0 && !three_pass_available(s)) return false;
   if (d == 2 && asm2_tile_for(s.fs.p, p->n_planes) == 0) return false;
   // TMA: 16-byte aligned rows and plane stride
   if ((s.fs.npt[0] * 8) % 16 != 0 || (p->plane_stride * 8) % 16 != 0 || p->n_planes > 256) return false;
@@ -1299,6 +1305,8 @@ ThreePass three_pass_plan(const AsmShape& s) {
   t.on = true;
   return t;
 }
+
+bool three_pass_available(const AsmShape& s) { return three_pass_plan(s).on; }
 
 size_t asm_workspace(const AsmShape& s) {
   const int W = 2 * s.fs.p - 1;
@@ -1539,7 +1547,6 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   ZRange z;
   IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
   const int tile = asm3_tile<P>(s.plan, p->n_planes);
-  if (tile == 0) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
   constexpr int W = 2 * P - 1;
   struct {
     int64_t NS0, NS1;
@@ -1547,7 +1554,8 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   // p >= 5: x and y contractions as separate passes (G chunks through HBM)
   // unless IGS_FLAG_TWO_PASS asks for the fused stage-1/2 kernel
   const ThreePass tp = three_pass_plan(s);
-  if (tp.on && tile < 4 && !two_pass) {
+  if (tile == 0 && !tp.on) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
+  if (tp.on && tile < 4 && (!two_pass || tile == 0)) {
     const int64_t nbh = ceil_div(a.NS0 * a.NS1, (int64_t)kSweepBlock);
     double* extra = H + (size_t)nbh * kSweepBlock * (z.sh - z.sl) * Q * s.plan.nh +
                     (size_t)s.fs.nel[2] * (Q * 4 * (P + 1) + 4);

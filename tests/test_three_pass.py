@@ -139,3 +139,39 @@ def test_three_pass_full_size_p5_chunks_vs_stage12(cuda):
     b = sumfac.assemble(prob, flags=TWO_PASS).values
     assert bool(torch.isfinite(a).all())
     assert float(torch.linalg.norm(a - b) / torch.linalg.norm(b)) <= 1e-13
+
+
+@pytest.mark.parametrize("p,K", [(5, (4, 3, 2)), (6, (2, 3, 2))])
+def test_three_pass_nonsymmetric_field(cuda, p, K):
+    """A full first-order coefficient field with 16 distinct planes
+    (reaction + convection in both slots + non-symmetric diffusion: A != Aᵀ):
+    the three-pass path takes any block plan whose stage-2 groups hold at
+    most 4 stage-1 groups; checked against the oracle's Kronecker assembly."""
+    import torch
+
+    sumfac, workloads = _mods()
+    from paper_1809_05471_b200.bspline import UnivariateBasis, uniform_open_knots
+    from paper_1809_05471_b200.geometry import CoefficientField, first_order_derivative_set
+    from paper_1809_05471_b200.quadrature import TensorQuadrature, per_element_rule
+
+    bases = [UnivariateBasis(uniform_open_knots(p, k)) for k in K]
+    quad = TensorQuadrature([per_element_rule(b.breakpoints, p) for b in bases])
+    npts = int(np.prod(quad.shape))
+    rng = np.random.default_rng(77)
+    planes_np = 1.0 + 0.3 * rng.standard_normal((16, npts))
+    plane_of = [[4 * i + j for j in range(4)] for i in range(4)]
+    ths = first_order_derivative_set(3)
+    field = CoefficientField.from_planes(ths, ths, torch.as_tensor(planes_np, device="cuda"), plane_of, quad.shape)
+    prob = sumfac.AssemblyProblem(bases, bases, quad, field)
+    assert sumfac.fused_path(prob) == 1
+    va = sumfac.assemble(prob).values_np()
+    vb = sumfac.assemble(prob, flags=TWO_PASS).values_np()
+    sp = [O.uniform_space(p, k) for k in K]
+    oths = O.first_order_set(3)
+    Ar = O.assemble_kron(sp, sp, oths, oths, O.dense_field(planes_np, plane_of))
+    pat = prob.pattern()
+    ref = O.values_on_pattern(Ar, pat.indptr, pat.indices)
+    assert _rel(va, ref) <= 1e-12
+    assert _rel(va, vb) <= 1e-12
+    S = sumfac.SparseMatrix(pat, torch.as_tensor(va, device="cuda")).to_scipy()
+    assert (S - S.T).count_nonzero() > 0  # genuinely non-symmetric
