@@ -887,7 +887,7 @@ bool pick(int P, int Q, Launch* L) {
   switch (P) {
     // p = 4: 8-row y tiles (16 warps) where they fit shared memory (measured
     // 1.51 -> 1.21 ms at 128^3, stiffness), else 4-row tiles (mass+stiffness)
-    case 2: *L = make_launch<2, 2, 8, 8, 2, MASS, STIFF>(); return true;
+    case 2: *L = make_launch<2, 2, 8, 12, 2, MASS, STIFF>(); return true;
     // p = 3: a single TMA stage lets two CTAs share an SM (18 warps):
     // 0.73 -> 0.66 ms at 128^3 (stiffness)
     case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF, 1>(); return true;
