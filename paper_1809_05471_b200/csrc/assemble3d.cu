@@ -1147,10 +1147,12 @@ int asm2_tile(int nplanes) {
 template <int P>
 size_t asm2_tables_bytes(int64_t nfn0) {
   const size_t t8 = (size_t)ceil_div(nfn0, 8) * A3Cfg<P, P, 8>::W0T;
+  const size_t t6 = (size_t)ceil_div(nfn0, 6) * A3Cfg<P, P, 6>::W0T;  // x-pass kernel (p >= 5)
   const size_t t4 = (size_t)ceil_div(nfn0, 4) * A3Cfg<P, P, 4>::W0T;
   const size_t t2 = (size_t)ceil_div(nfn0, 2) * A3Cfg<P, P, 2>::W0T;
   const size_t t1 = (size_t)nfn0 * A3Cfg<P, P, 1>::W0T;
   size_t m = t8 > t4 ? t8 : t4;
+  m = m > t6 ? m : t6;
   m = m > t2 ? m : t2;
   m = m > t1 ? m : t1;
   return m * sizeof(double);
@@ -1675,12 +1677,48 @@ igs_status launch2_stage1(const igs_problem* p, const AsmShape& s, const double*
   return IGS_OK;
 }
 
+// 2D x pass through asm3_xpass (one "layer": the rows are the y points).
+template <int P, int Q, int T>
+igs_status launch2_xpass(const igs_problem* p, const AsmShape& s, const double* planes, double* G,
+                         cudaStream_t st) {
+  using C = A3Cfg<P, Q, T>;
+  if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
+  CUtensorMap fmap;
+  {
+    const int64_t dims[4] = {s.fs.npt[0], s.fs.npt[1], 1, p->n_planes};
+    const unsigned box[4] = {(unsigned)AXCfg<P, Q, T>::XB, (unsigned)A3P_YS, 1u, (unsigned)p->n_planes};
+    IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
+  }
+  // band tables behind the G region and the last-direction element records (as launch2_stage1)
+  const int64_t nbsp = ceil_div(s.fs.nfn[0] * C::W, (int64_t)kSweepBlock);
+  double* Wg = G + (size_t)nbsp * kSweepBlock * s.fs.npt[1] * s.plan.ng +
+               (((size_t)s.fs.nel[1] * S3Cfg<P, Q>::NWR + 1) & ~size_t(1));
+  const int nt0 = (int)ceil_div(s.fs.nfn[0], T);
+  asm2_tables_kernel<P, Q, T><<<(unsigned)nt0, 256, 0, st>>>(tab_args(p), Wg);
+  IGS_LAUNCH_CHECK("asm2_tables_kernel");
+  return launch3_passA<P, Q, T>(p, s, fmap, Wg, G, 0, 1, st);
+}
+
 template <int P, int Q>
 igs_status launch2(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
                    const int64_t* base, const double* planes, double* values, double* G, cudaStream_t st,
                    bool kernel_only) {
   constexpr int W = 2 * P - 1;
-  switch (asm2_tile<P>(p->n_planes)) {
+  bool xdone = false;
+  if constexpr (P >= 5) {
+    // p >= 5: the 16-row-box x-pass kernel of the 3D three-pass path fits a
+    // wider x tile than asm2_stage1's 64-row boxes (p = 6: 4 rows instead of 2)
+    const int tx = three_pass_tile<P>(p->n_planes);
+    if (tx > asm2_tile<P>(p->n_planes)) {
+      switch (tx) {
+        case 6: IGS_TRY((launch2_xpass<P, Q, 6>(p, s, planes, G, st))); break;
+        case 4: IGS_TRY((launch2_xpass<P, Q, 4>(p, s, planes, G, st))); break;
+        default: IGS_TRY((launch2_xpass<P, Q, 2>(p, s, planes, G, st))); break;
+      }
+      xdone = true;
+    }
+  }
+  if (!xdone) switch (asm2_tile<P>(p->n_planes)) {
     case 8: IGS_TRY((launch2_stage1<P, Q, 8>(p, s, planes, G, st))); break;
     case 4: IGS_TRY((launch2_stage1<P, Q, 4>(p, s, planes, G, st))); break;
     case 2: IGS_TRY((launch2_stage1<P, Q, 2>(p, s, planes, G, st))); break;
