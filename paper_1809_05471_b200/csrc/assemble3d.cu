@@ -203,9 +203,12 @@ __host__ __device__ __forceinline__ int64_t sweep_offset(int64_t sp, int64_t e_l
 
 // Stage-1/2 tile plan: T x T rows in (x, y), their (T+P-1)-element support
 // region, slots = T·(2P-1) band entries per direction.
-template <int P, int Q, int T>
+// SYM: only the x-pairs n0 >= m0 (slots m·P + (n - m), the symmetric half of
+// the band; three-pass path of a symmetric problem, mirrored in the z sweep).
+template <int P, int Q, int T, bool SYM = false>
 struct A3Cfg {
-  static constexpr int W = 2 * P - 1;        // band width
+  static constexpr int W = SYM ? P : 2 * P - 1;  // slots per row: band width (or its symmetric half)
+  static constexpr int OFF = SYM ? 0 : P - 1;    // slot offset of the diagonal (n = m)
   // slot positions per row: a 7-wide band is padded to 8 so every MMA slot
   // tile is exactly one row (its k-range is then exactly the row's P elements)
   static constexpr int SR = W == 7 ? 8 : W;
@@ -235,9 +238,9 @@ struct A3Cfg {
 // v = θ + 2η; zero where x is outside the mesh/region or (m, n) outside the
 // support of x's element (same product order as _Core.w_matrix).
 // transposed = true stores [v][s][x] (row pitch YP) for the stage-2 A operand.
-template <int P, int Q, int T, bool TRANSPOSED>
+template <int P, int Q, int T, bool TRANSPOSED, bool SYM = false>
 __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row, int64_t x_first) {
-  using C = A3Cfg<P, Q, T>;
+  using C = A3Cfg<P, Q, T, SYM>;
   constexpr int W = C::W;
   constexpr int NX = TRANSPOSED ? C::XRP : C::XK;
   constexpr int NS = TRANSPOSED ? C::PTP : C::SP;
@@ -251,7 +254,7 @@ __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row
     double val = 0.0;
     if (xl < C::XR && xl < NX && sl < C::PT && sl < NS && sl % C::SR < W) {
       const int64_t x = x_first + xl;
-      const int64_t m = a_row + sl / C::SR, n = m + sl % C::SR - (P - 1);
+      const int64_t m = a_row + sl / C::SR, n = m + sl % C::SR - C::OFF;
       if (x >= 0 && x < t.X[dir] && m < Nf && n >= 0 && n < Nf) {
         const int64_t e = x / Q;
         const int64_t jn = n - e, jm = m - e;
@@ -270,9 +273,9 @@ __device__ void fill_band_table(double* Wt, const TabArgs& t, int dir, int a_row
 
 // k-steps (of 4 points) of the region that touch the tile rows behind slot
 // tile `st`: row r (tile-relative) is supported by region elements [r, r+P-1].
-template <int P, int Q, int T>
+template <int P, int Q, int T, bool SYM = false>
 __host__ __device__ constexpr void slot_tile_ksteps(int st, int kmax, int& k_lo, int& k_hi) {
-  constexpr int SR = A3Cfg<P, Q, T>::SR;
+  constexpr int SR = A3Cfg<P, Q, T, SYM>::SR;
   const int r_lo = (st * 8) / SR;
   const int r_hi = (st * 8 + 7) / SR < T - 1 ? (st * 8 + 7) / SR : T - 1;
   k_lo = (r_lo * Q) / 4;
@@ -290,12 +293,12 @@ constexpr int min_ksteps(int ntiles, int kmax) {
   return m;
 }
 // longest k-step range over the slot tiles (static unroll bound)
-template <int P, int Q, int T>
+template <int P, int Q, int T, bool SYM = false>
 constexpr int max_ksteps(int ntiles, int kmax) {
   int m = 1;
   for (int st = 0; st < ntiles; ++st) {
     int lo = 0, hi = 0;
-    slot_tile_ksteps<P, Q, T>(st, kmax, lo, hi);
+    slot_tile_ksteps<P, Q, T, SYM>(st, kmax, lo, hi);
     if (hi - lo > m) m = hi - lo;
   }
   return m;
@@ -506,10 +509,16 @@ struct S3Cfg {
 // P-1 elements early (its first rows are then complete) and writes the rows
 // of its own elements (the last chunk also the trailing P-1 rows).  2D is
 // 3D with a trivial middle direction.
-template <int P, int Q, int D>
+// SYMX (3D three-pass path of a symmetric problem, whole matrix): the x slots
+// hold only n0 >= m0 (s0 = m0·P + (n0 - m0)); a pair with n0 > m0 writes each
+// value to its own row and, mirrored, to row (n0, n1, n2) at column
+// (m0, m1, m2) — every CSR entry exactly once.
+template <int P, int Q, int D, bool SYMX = false>
 __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs a) {
   using C = S3Cfg<P, Q>;
   constexpr int W = 2 * P - 1, NWT = C::NWT, NWR = C::NWR, PP = C::PP, L = D - 1;
+  constexpr int WX = SYMX ? P : W, OFFX = SYMX ? 0 : P - 1;
+  static_assert(!SYMX || D == 3, "mirrored sweep: 3D only");
   static_assert(NWT % 2 == 0, "16-byte table chunks");
   extern __shared__ __align__(16) double s3[];
   double* hst = s3;                    // [NS3][Q][ngrp][NT3]
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
   const int64_t sp = sb * NT3 + tid;
   const int64_t s0 = sp % a.NS0, s1 = sp / a.NS0;
   const int64_t N0 = a.tab.N[0], N1 = D == 3 ? a.tab.N[1] : 1, N2 = a.tab.N[L];
-  const int64_t m0 = s0 / W, n0 = m0 + (s0 % W) - (P - 1);
+  const int64_t m0 = s0 / WX, n0 = m0 + (s0 % WX) - OFFX;
   const int64_t m1 = D == 3 ? s1 / W : 0, n1 = D == 3 ? m1 + (s1 % W) - (P - 1) : 0;
   const bool valid = sp < npairs && n0 >= 0 && n0 < N0 && n1 >= 0 && n1 < N1 && m0 < N0 && m1 < N1;
   // CSR geometry of this thread's (row, column) pairs in the first directions
@@ -540,6 +549,17 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       P1 = a.pat.rp[1][N1];
       r1 = n1 - a.pat.cl[1][rp1];
     }
+  }
+  // mirror geometry: row (n0, n1, ·), column (m0, m1, ·)
+  const bool mir = SYMX && valid && n0 > m0;
+  int64_t w0n = 1, w1n = 1, rp0n = 0, rp1n = 0, r0n = 0, r1n = 0;
+  if (mir) {
+    rp0n = a.pat.rp[0][n0];
+    w0n = a.pat.rp[0][n0 + 1] - rp0n;
+    r0n = m0 - a.pat.cl[0][rp0n];
+    rp1n = a.pat.rp[1][n1];
+    w1n = a.pat.rp[1][n1 + 1] - rp1n;
+    r1n = m1 - a.pat.cl[1][rp1n];
   }
   double ring[P][W];
 #pragma unroll
@@ -564,6 +584,19 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
     for (int k = 0; k < W; ++k) {
       const int64_t n2 = m2 + k - (P - 1);
       if (n2 >= 0 && n2 < N2) a.values[start + (n2 - lo2) * w0 * w1 + r1 * w0 + r0] = row[k];
+    }
+    if (mir) {
+      // (SYMX runs whole-matrix ranges only: every mirrored row is in range)
+      const int64_t* rpz = a.pat.rp[L];
+      const int64_t* clz = a.pat.cl[L];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const int64_t n2 = m2 + k - (P - 1);
+        if (n2 < 0 || n2 >= N2) continue;
+        const int64_t rp2n = rpz[n2], w2n = rpz[n2 + 1] - rp2n, lo2n = clz[rp2n];
+        const int64_t startn = rp0n * w1n * w2n + P0 * rp1n * w2n + P0 * P1 * rp2n - base;
+        a.values[startn + (m2 - lo2n) * w0n * w1n + r1n * w0n + r0n] = row[k];
+      }
     }
   };
   const unsigned htile = (unsigned)(Q * nh * NT3 * sizeof(double));
@@ -861,11 +894,11 @@ struct Asm2Args {
 // The 2D tiles' band tables, one block per row tile, built once per
 // assembly: the stage-1 CTAs (several per tile, one per y chunk) then
 // bulk-copy theirs instead of recomputing it.
-template <int P, int Q, int T>
+template <int P, int Q, int T, bool SYM = false>
 __global__ void asm2_tables_kernel(const TabArgs tab, double* Wg) {
-  using C = A3Cfg<P, Q, T>;
+  using C = A3Cfg<P, Q, T, SYM>;
   const int a0 = blockIdx.x * T;
-  fill_band_table<P, Q, T, false>(Wg + (size_t)blockIdx.x * C::W0T, tab, 0, a0, (a0 - (P - 1)) * Q);
+  fill_band_table<P, Q, T, false, SYM>(Wg + (size_t)blockIdx.x * C::W0T, tab, 0, a0, (a0 - (P - 1)) * Q);
 }
 
 // 2D stage 1 as a dense banded GEMM on DMMA (the 3D stage-1 structure):
@@ -980,9 +1013,9 @@ __global__ void __launch_bounds__(A2_NT) asm2_stage1(const Asm2Args a, const __g
 //     tiles of the box: every warp has a task in every stage (12-14 tasks on
 //     16 warps left a quarter of the CTA idle at the stage barrier) and each
 //     W fragment feeds two DMMAs (3 fragment loads per 2 MMAs).
-template <int P, int Q, int T>
+template <int P, int Q, int T, bool SYM = false>
 struct AXCfg {
-  using B = A3Cfg<P, Q, T>;
+  using B = A3Cfg<P, Q, T, SYM>;
   static constexpr int YS = 16;
   static constexpr int xb() {
     int b = B::XK;  // >= the region width, covers the k-step tail
@@ -998,15 +1031,15 @@ struct AXCfg {
   static_assert(XB <= 256 && XB >= B::XK, "TMA box / k-step tail");
 };
 
-template <int P, int Q, int T>
-__global__ void __launch_bounds__(AXCfg<P, Q, T>::NT) asm3_xpass(const Asm2Args a,
-                                                                  const __grid_constant__ CUtensorMap fmap,
-                                                                  int nplanes) {
-  using C = A3Cfg<P, Q, T>;
-  using CX = AXCfg<P, Q, T>;
+template <int P, int Q, int T, bool SYM = false>
+__global__ void __launch_bounds__(AXCfg<P, Q, T, SYM>::NT) asm3_xpass(const Asm2Args a,
+                                                                       const __grid_constant__ CUtensorMap fmap,
+                                                                       int nplanes) {
+  using C = A3Cfg<P, Q, T, SYM>;
+  using CX = AXCfg<P, Q, T, SYM>;
   constexpr int PT = C::PT, PTP = C::PTP, XK = C::XK, SP = C::SP, W = C::W, SR = C::SR;
   constexpr int YS = CX::YS, XB = CX::XB, NT = CX::NT, NW = CX::NW;
-  constexpr int KL = max_ksteps<P, Q, T>(PTP / 8, XK / 4);
+  constexpr int KL = max_ksteps<P, Q, T, SYM>(PTP / 8, XK / 4);
   constexpr int NST = PTP / 8;
   extern __shared__ __align__(128) double sm[];
   const AsmPlan& pl = a.plan;
@@ -1047,7 +1080,7 @@ __global__ void __launch_bounds__(AXCfg<P, Q, T>::NT) asm3_xpass(const Asm2Args 
     for (int t = warp; t < CX::NTASK; t += NW) {
       const int half = t & 1, st = t >> 1;
       int k_lo, k_hi;
-      slot_tile_ksteps<P, Q, T>(st, XK / 4, k_lo, k_hi);
+      slot_tile_ksteps<P, Q, T, SYM>(st, XK / 4, k_lo, k_hi);
       const double* Fy = Fb0 + g8 * XB + m4 + k_lo * 4;  // y tile 0; tile 1 at + 8·XB
       const double* Wk = W0 + (m4 + k_lo * 4) * SP + st * 8 + g8;
       const int s = st * 8 + 2 * m4;
@@ -1408,10 +1441,10 @@ igs_status launch3_stage12(const igs_problem* p, const AsmShape& s, const ZRange
 
 // Pass A of the three-pass path for one chunk of z layers [zc0, zc0 + nz):
 // asm2_stage1 over the chunk's rows (layer-major, y fastest).
-template <int P, int Q, int T>
+template <int P, int Q, int T, bool SYM = false>
 igs_status launch3_passA(const igs_problem* p, const AsmShape& s, const CUtensorMap& fmap, const double* Wg,
                          double* G, int64_t ytma0, int64_t nz, cudaStream_t st) {
-  using C = A3Cfg<P, Q, T>;
+  using C = A3Cfg<P, Q, T, SYM>;
   Asm2Args a{};
   a.plan = s.plan;
   a.tab = tab_args(p);
@@ -1422,16 +1455,16 @@ igs_status launch3_passA(const igs_problem* p, const AsmShape& s, const CUtensor
   a.ytma0 = ytma0;
   a.nt0 = (int)ceil_div(s.fs.nfn[0], T);
   a.Wg = Wg;
-  using CX = AXCfg<P, Q, T>;
+  using CX = AXCfg<P, Q, T, SYM>;
   const size_t smem = CX::smem(p->n_planes);
   static std::atomic<int> res_cache[17];
   const int npl_key = p->n_planes < 0 ? 0 : (p->n_planes > 16 ? 16 : p->n_planes);
   int resident = res_cache[npl_key].load(std::memory_order_relaxed);
-  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_xpass<P, Q, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  IGS_TRY(cuda_check(cudaFuncSetAttribute(asm3_xpass<P, Q, T, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem),
                      "smem attribute"));
   if (resident <= 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm3_xpass<P, Q, T>, CX::NT, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, asm3_xpass<P, Q, T, SYM>, CX::NT, smem) !=
             cudaSuccess ||
         resident < 1) {
       cudaGetLastError();
@@ -1456,17 +1489,17 @@ igs_status launch3_passA(const igs_problem* p, const AsmShape& s, const CUtensor
   }
   a.yc = (int)(per_best * A3P_YS);
   const int64_t nyc = ceil_div(a.X1, (int64_t)a.yc);
-  asm3_xpass<P, Q, T><<<(unsigned)(a.nt0 * nyc), CX::NT, smem, st>>>(a, fmap, p->n_planes);
+  asm3_xpass<P, Q, T, SYM><<<(unsigned)(a.nt0 * nyc), CX::NT, smem, st>>>(a, fmap, p->n_planes);
   IGS_LAUNCH_CHECK("asm3_xpass");
   return IGS_OK;
 }
 
-template <int P, int Q, int T>
+template <int P, int Q, int T, bool SYM>
 igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const ThreePass& tp, const ZRange& z,
                                 TensorPat pat, const double* planes, double* H, double* extra,
                                 cudaStream_t st) {
-  using C = A3Cfg<P, Q, T>;
-  constexpr int W = 2 * P - 1;
+  using C = A3Cfg<P, Q, T, SYM>;
+  constexpr int W = C::W;  // x slots per row (the symmetric half for SYM)
   if (((uintptr_t)planes & 15) != 0) return fail(IGS_EARG, "coefficient planes must be 16-byte aligned");
   double* w1g = extra;
   double* G = w1g + tp.w1_doubles;
@@ -1476,12 +1509,12 @@ igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const T
   {
     // rows = (layer of the held planes, y) flattened
     const int64_t dims[4] = {s.fs.npt[0], ny * (int64_t)(z.sh - z.sl) * Q, 1, p->n_planes};
-    const unsigned box[4] = {(unsigned)AXCfg<P, Q, T>::XB, (unsigned)A3P_YS, 1u, (unsigned)p->n_planes};
+    const unsigned box[4] = {(unsigned)AXCfg<P, Q, T, SYM>::XB, (unsigned)A3P_YS, 1u, (unsigned)p->n_planes};
     IGS_TRY(planes_tensor_map(&fmap, planes, dims, p->plane_stride, box));
   }
   const TabArgs tab = tab_args(p);
   const int nt0 = (int)ceil_div(s.fs.nfn[0], T);
-  asm2_tables_kernel<P, Q, T><<<(unsigned)nt0, 256, 0, st>>>(tab, Wg);
+  asm2_tables_kernel<P, Q, T, SYM><<<(unsigned)nt0, 256, 0, st>>>(tab, Wg);
   IGS_LAUNCH_CHECK("asm2_tables_kernel");
   {
     Asm3bArgs b{};
@@ -1516,7 +1549,7 @@ igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const T
   const unsigned nbs0 = (unsigned)ceil_div(y.NS0, (int64_t)kSweepBlock);
   for (int64_t zc = z0; zc < z1; zc += tp.nzc) {
     const int64_t nz = min64(tp.nzc, z1 - zc);
-    IGS_TRY((launch3_passA<P, Q, T>(p, s, fmap, Wg, G, (zc - zpl) * ny, nz, st)));
+    IGS_TRY((launch3_passA<P, Q, T, SYM>(p, s, fmap, Wg, G, (zc - zpl) * ny, nz, st)));
     y.NE_G = nz * s.fs.nel[1];
     y.zrel0 = zc - z0;
     dim3 grid(nbs0, (unsigned)nz, (unsigned)s.plan.nh);
@@ -1528,13 +1561,21 @@ igs_status launch3_three_pass_T(const igs_problem* p, const AsmShape& s, const T
 
 template <int P, int Q>
 igs_status launch3_three_pass(const igs_problem* p, const AsmShape& s, const ThreePass& tp, const ZRange& z,
-                              TensorPat pat, const double* planes, double* H, double* extra, cudaStream_t st) {
+                              TensorPat pat, const double* planes, double* H, double* extra, cudaStream_t st,
+                              bool sym) {
   if constexpr (P >= 5) {
-    switch (tp.T) {
-      case 6: return launch3_three_pass_T<P, Q, 6>(p, s, tp, z, pat, planes, H, extra, st);
-      case 4: return launch3_three_pass_T<P, Q, 4>(p, s, tp, z, pat, planes, H, extra, st);
-      case 2: return launch3_three_pass_T<P, Q, 2>(p, s, tp, z, pat, planes, H, extra, st);
-      case 1: return launch3_three_pass_T<P, Q, 1>(p, s, tp, z, pat, planes, H, extra, st);
+    if (sym) switch (tp.T) {
+      case 6: return launch3_three_pass_T<P, Q, 6, true>(p, s, tp, z, pat, planes, H, extra, st);
+      case 4: return launch3_three_pass_T<P, Q, 4, true>(p, s, tp, z, pat, planes, H, extra, st);
+      case 2: return launch3_three_pass_T<P, Q, 2, true>(p, s, tp, z, pat, planes, H, extra, st);
+      case 1: return launch3_three_pass_T<P, Q, 1, true>(p, s, tp, z, pat, planes, H, extra, st);
+      default: break;
+    }
+    else switch (tp.T) {
+      case 6: return launch3_three_pass_T<P, Q, 6, false>(p, s, tp, z, pat, planes, H, extra, st);
+      case 4: return launch3_three_pass_T<P, Q, 4, false>(p, s, tp, z, pat, planes, H, extra, st);
+      case 2: return launch3_three_pass_T<P, Q, 2, false>(p, s, tp, z, pat, planes, H, extra, st);
+      case 1: return launch3_three_pass_T<P, Q, 1, false>(p, s, tp, z, pat, planes, H, extra, st);
       default: break;
     }
   }
@@ -1550,18 +1591,23 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
   const int tile = asm3_tile<P>(s.plan, p->n_planes);
   constexpr int W = 2 * P - 1;
-  struct {
-    int64_t NS0, NS1;
-  } a{s.fs.nfn[0] * W, s.fs.nfn[1] * W};
   // p >= 5: x and y contractions as separate passes (G chunks through HBM)
   // unless IGS_FLAG_TWO_PASS asks for the fused stage-1/2 kernel
   const ThreePass tp = three_pass_plan(s);
   if (tile == 0 && !tp.on) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
-  if (tp.on && tile < 4 && (!two_pass || tile == 0)) {
+  const bool three = tp.on && tile < 4 && (!two_pass || tile == 0);
+  // A = Aᵀ (whole matrix, whole-grid planes): only the x-pairs n0 >= m0 go
+  // through the passes; the z sweep writes each value and its mirror
+  const bool symx = three && problem_symmetric(p) && !(p->slab_lo || p->slab_hi) && row_lo == 0 &&
+                    row_hi == s.fs.nfn[0] * s.fs.nfn[1] * s.fs.nfn[2];
+  struct {
+    int64_t NS0, NS1;
+  } a{s.fs.nfn[0] * (symx ? P : W), s.fs.nfn[1] * W};
+  if (three) {
     const int64_t nbh = ceil_div(a.NS0 * a.NS1, (int64_t)kSweepBlock);
     double* extra = H + (size_t)nbh * kSweepBlock * (z.sh - z.sl) * Q * s.plan.nh +
                     (size_t)s.fs.nel[2] * (Q * 4 * (P + 1) + 4);
-    IGS_TRY((launch3_three_pass<P, Q>(p, s, tp, z, pat, planes, H, extra, st)));
+    IGS_TRY((launch3_three_pass<P, Q>(p, s, tp, z, pat, planes, H, extra, st, symx)));
   } else {
     if constexpr (kWideTile<P> > 0) {
       if (tile == kWideTile<P>) IGS_TRY((launch3_stage12<P, Q, kWideTile<P>>(p, s, z, planes, H, st)));
@@ -1600,6 +1646,16 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   }
   b.NE = z.e_hi - z.e_lo;
   constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
+  if constexpr (P >= 5) {
+    if (symx) {
+      IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 3, true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3),
+                         "smem attribute"));
+      asm_sweep<P, Q, 3, true><<<(unsigned)nbsp, NT3, smem3, st>>>(b);
+      IGS_LAUNCH_CHECK("asm_sweep<3, sym>");
+      return IGS_OK;
+    }
+  }
   IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem3),
                      "smem attribute"));
