@@ -589,6 +589,17 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       // (SYMX runs whole-matrix ranges only: every mirrored row is in range)
       const int64_t* rpz = a.pat.rp[L];
       const int64_t* clz = a.pat.cl[L];
+      if (m2 >= 2 * (P - 1) && m2 + 2 * P - 1 <= N2) {
+        // every row n2 within P-1 of m2 is an interior z row (width W, first
+        // column n2 - (P-1), row starts W apart): the mirror offsets are affine in k
+        const int64_t ww = w0n * w1n;
+        const int64_t rz = rpz[P - 1] + (m2 - 2 * (P - 1)) * W;  // row start of n2 = m2 - (P-1)
+        double* vm = a.values + ((rp0n * w1n + P0 * rp1n) * W + P0 * P1 * rz - base + 2 * (P - 1) * ww +
+                                 r1n * w0n + r0n);
+        const int64_t step = P0 * P1 * W - ww;
+#pragma unroll
+        for (int k = 0; k < W; ++k) vm[k * step] = row[k];
+      } else
 #pragma unroll
       for (int k = 0; k < W; ++k) {
         const int64_t n2 = m2 + k - (P - 1);
