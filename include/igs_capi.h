@@ -111,8 +111,11 @@ enum {
                                    intermediate H in HBM) even where the one-pass
                                    symmetric kernel (3D p = 2, 4; 2D) or the three-pass
                                    path (3D p = 5, 6) applies                            */
-  IGS_FLAG_SPLIT_BOUNDARY = 16  /* igs_apply_sharded: interior / boundary launches even
+  IGS_FLAG_SPLIT_BOUNDARY = 16, /* igs_apply_sharded: interior / boundary launches even
                                    without a next rank (exercises the overlap path)     */
+  IGS_FLAG_THREE_PASS = 32      /* assembly, 3D p = 3..6: one direction per pass (x on
+                                   DMMA, y and z sweeps; G and H in the workspace) even
+                                   where another fused kernel is the default (p = 4)    */
 };
 
 /* ---- diagnostics ---------------------------------------------------- */

@@ -21,7 +21,7 @@ MAX_ORDER = 16
 
 OP_ASSEMBLE, OP_APPLY, OP_EVAL_FIELD, OP_PATTERN = 1, 2, 3, 4
 FLAG_DEFAULT, FLAG_FORCE_GENERIC, FLAG_ACCUMULATE = 0, 1, 2
-FLAG_KERNEL_ONLY, FLAG_TWO_PASS, FLAG_SPLIT_BOUNDARY = 4, 8, 16
+FLAG_KERNEL_ONLY, FLAG_TWO_PASS, FLAG_SPLIT_BOUNDARY, FLAG_THREE_PASS = 4, 8, 16, 32
 
 IGS_OK, IGS_EARG, IGS_EDOMAIN, IGS_EDERIV, IGS_ECAPACITY, IGS_ECUDA, IGS_ENCCL, IGS_EWORKSPACE = range(8)
 

@@ -1330,11 +1330,12 @@ size_t three_pass_table_doubles(int T, int64_t nfn0) {
 
 ThreePass three_pass_plan(const AsmShape& s) {
   ThreePass t{};
-  if (s.fs.d != 3 || s.fs.p < 5) return t;
+  if (s.fs.d != 3 || s.fs.p < 3) return t;
   for (int h = 0; h < s.plan.nh; ++h)
     if (s.plan.h_ng[h] > 4) return t;
   if (s.plan.nh > 4) return t;
-  t.T = s.fs.p == 5 ? three_pass_tile<5>(s.nplanes) : three_pass_tile<6>(s.nplanes);
+  t.T = s.fs.p == 3 ? three_pass_tile<3>(s.nplanes) : s.fs.p == 4 ? three_pass_tile<4>(s.nplanes)
+        : s.fs.p == 5 ? three_pass_tile<5>(s.nplanes) : three_pass_tile<6>(s.nplanes);
   if (t.T == 0) return t;
   const int W = 2 * s.fs.p - 1;
   const size_t s0pad = (size_t)ceil_div(s.fs.nfn[0] * W, (int64_t)kSweepBlock) * kSweepBlock;
@@ -1346,8 +1347,10 @@ ThreePass three_pass_plan(const AsmShape& s) {
   t.g_doubles = per_layer * nzc;
   const int PP = (s.fs.p + 1) & ~1;
   t.w1_doubles = ((size_t)s.fs.nel[1] * (s.fs.k * 4 * PP + 4) + 1) & ~size_t(1);
-  t.wg_doubles = s.fs.p == 5 ? three_pass_table_doubles<5>(t.T, s.fs.nfn[0])
-                             : three_pass_table_doubles<6>(t.T, s.fs.nfn[0]);
+  t.wg_doubles = s.fs.p == 3   ? three_pass_table_doubles<3>(t.T, s.fs.nfn[0])
+                 : s.fs.p == 4 ? three_pass_table_doubles<4>(t.T, s.fs.nfn[0])
+                 : s.fs.p == 5 ? three_pass_table_doubles<5>(t.T, s.fs.nfn[0])
+                               : three_pass_table_doubles<6>(t.T, s.fs.nfn[0]);
   t.on = true;
   return t;
 }
@@ -1574,7 +1577,7 @@ template <int P, int Q>
 igs_status launch3_three_pass(const igs_problem* p, const AsmShape& s, const ThreePass& tp, const ZRange& z,
                               TensorPat pat, const double* planes, double* H, double* extra, cudaStream_t st,
                               bool sym) {
-  if constexpr (P >= 5) {
+  if constexpr (P >= 3) {
     if (sym) switch (tp.T) {
       case 6: return launch3_three_pass_T<P, Q, 6, true>(p, s, tp, z, pat, planes, H, extra, st);
       case 4: return launch3_three_pass_T<P, Q, 4, true>(p, s, tp, z, pat, planes, H, extra, st);
@@ -1596,7 +1599,7 @@ igs_status launch3_three_pass(const igs_problem* p, const AsmShape& s, const Thr
 template <int P, int Q>
 igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64_t row_lo, int64_t row_hi,
                    const int64_t* base, const double* planes, double* values, double* H, cudaStream_t st,
-                   bool kernel_only, bool two_pass) {
+                   bool kernel_only, bool two_pass, bool force3) {
   if (row_hi <= row_lo) return IGS_OK;
   ZRange z;
   IGS_TRY(z_range(p, s, row_lo, row_hi, &z));
@@ -1606,11 +1609,16 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   // unless IGS_FLAG_TWO_PASS asks for the fused stage-1/2 kernel
   const ThreePass tp = three_pass_plan(s);
   if (tile == 0 && !tp.on) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
-  const bool three = tp.on && tile < 4 && (!two_pass || tile == 0);
   // A = Aᵀ (whole matrix, whole-grid planes): only the x-pairs n0 >= m0 go
   // through the passes; the z sweep writes each value and its mirror
-  const bool symx = three && problem_symmetric(p) && !(p->slab_lo || p->slab_hi) && row_lo == 0 &&
-                    row_hi == s.fs.nfn[0] * s.fs.nfn[1] * s.fs.nfn[2];
+  const bool sym_whole = problem_symmetric(p) && !(p->slab_lo || p->slab_hi) && row_lo == 0 &&
+                         row_hi == s.fs.nfn[0] * s.fs.nfn[1] * s.fs.nfn[2];
+  // p = 3: the symmetric three-pass path beats the stage-1/2 kernel (0.83 vs
+  // 1.02 ms at 64^3 M+K; its 5-wide band wastes the 8-wide MMA tiles of both
+  // stages); p = 4 keeps the one-pass / stage-1/2 kernels (three-pass 1.99 ms
+  // vs 1.50 ms: G and H through HBM); IGS_FLAG_THREE_PASS forces it
+  const bool three = tp.on && (tile < 4 || force3 || (P == 3 && sym_whole)) && (!two_pass || tile == 0);
+  const bool symx = three && sym_whole;
   struct {
     int64_t NS0, NS1;
   } a{s.fs.nfn[0] * (symx ? P : W), s.fs.nfn[1] * W};
@@ -1657,7 +1665,7 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   }
   b.NE = z.e_hi - z.e_lo;
   constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
-  if constexpr (P >= 5) {
+  if constexpr (P >= 3) {
     if (symx) {
       IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 3, true>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3),
@@ -1883,7 +1891,7 @@ size_t fused_assemble_workspace(const igs_problem* p, const Dims& D, int flags) 
   // whole-grid coefficients: the one-pass kernel covers every row range and
   // needs only the row-offset scalar; a slab may need the two-kernel path
   const bool slab = p->slab_lo || p->slab_hi;
-  if (!slab && !(flags & IGS_FLAG_TWO_PASS) && sym_eligible(p, s)) return 512;
+  if (!slab && !(flags & (IGS_FLAG_TWO_PASS | IGS_FLAG_THREE_PASS)) && sym_eligible(p, s)) return 512;
   return asm_workspace(s);
 }
 
@@ -1929,7 +1937,7 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
     IGS_LAUNCH_CHECK("row_start_kernel");
     return IGS_OK;
   };
-  if (sym_eligible(p, s) && !(flags & IGS_FLAG_TWO_PASS)) {
+  if (sym_eligible(p, s) && !(flags & (IGS_FLAG_TWO_PASS | IGS_FLAG_THREE_PASS))) {
     const bool slab = p->slab_lo || p->slab_hi;
     const int sl = slab ? p->slab_lo : 0, sh = slab ? p->slab_hi : (int)s.fs.nel[2];
     if (row_lo != 0) IGS_TRY(set_base());
@@ -1949,7 +1957,8 @@ igs_status fused_assemble(const igs_problem* p, const Dims& D, const int64_t* co
 #define IGS_ASM_CASE(PP, QQ)                                                                    \
   if (!done && P == PP && Q == QQ) {                                                            \
     r = p->d == 3 ? launch3<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko,   \
-                                     (flags & IGS_FLAG_TWO_PASS) != 0)                            \
+                                     (flags & IGS_FLAG_TWO_PASS) != 0,                           \
+                                     (flags & IGS_FLAG_THREE_PASS) != 0)                          \
                   : launch2<PP, QQ>(p, s, pat, row_lo, row_hi, base, planes, values, buf, st, ko);  \
     done = true;                                                                                \
   }

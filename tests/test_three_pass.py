@@ -19,7 +19,7 @@ from oracle import igs_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-TWO_PASS, GENERIC = 8, 1
+TWO_PASS, GENERIC, THREE_PASS = 8, 1, 32
 
 
 def _mods():
@@ -47,6 +47,8 @@ def _rel(a, b):
 @pytest.mark.parametrize("p,K,kind", [
     (5, (2, 1, 1), 1), (5, (4, 3, 2), 3), (5, (6, 7, 5), 2), (5, (14, 3, 4), 3), (5, (2, 9, 3), 2),
     (6, (1, 1, 1), 3), (6, (2, 2, 3), 3), (6, (5, 4, 3), 2), (6, (9, 2, 2), 3), (6, (3, 7, 2), 1),
+    # p = 3: the symmetric three-pass path is the default for whole symmetric matrices
+    (3, (2, 1, 1), 3), (3, (8, 6, 7), 2), (3, (14, 5, 9), 3), (3, (4, 13, 2), 1),
 ])
 def test_three_pass_vs_oracle_stage12_generic(cuda, p, K, kind):
     sumfac, workloads = _mods()
@@ -175,3 +177,17 @@ def test_three_pass_nonsymmetric_field(cuda, p, K):
     assert _rel(va, vb) <= 1e-12
     S = sumfac.SparseMatrix(pat, torch.as_tensor(va, device="cuda")).to_scipy()
     assert (S - S.T).count_nonzero() > 0  # genuinely non-symmetric
+
+
+@pytest.mark.parametrize("p,K,kind", [(3, (8, 5, 6), 3), (4, (6, 5, 7), 3), (4, (13, 4, 6), 2), (5, (4, 3, 2), 3)])
+def test_three_pass_flag_forces_the_path(cuda, p, K, kind):
+    """IGS_FLAG_THREE_PASS: the three-pass path at every instantiated order
+    (p = 4 defaults to the one-pass kernel) equals the default path."""
+    sumfac, workloads = _mods()
+    prob, _ = _problem(p, K, kind, seed=63)
+    va = sumfac.assemble(prob).values_np()
+    vt = sumfac.assemble(prob, flags=THREE_PASS).values_np()
+    vb = sumfac.assemble(prob, flags=TWO_PASS).values_np()
+    assert np.all(np.isfinite(vt))
+    assert _rel(vt, va) <= 1e-12
+    assert _rel(vt, vb) <= 1e-12
