@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
   double* hst = s3;                    // [NS3][Q][ngrp][NT3]
   double* w2s = s3 + NS3 * C::HST;     // [NS3][NWR]: factors [Q][4][P] + row metadata
   uint64_t* bars = reinterpret_cast<uint64_t*>(w2s + NS3 * NWR);
+  int64_t* zrt = reinterpret_cast<int64_t*>(bars + NS3);  // SYMX: [N2][3] z-row table
   const int nh = a.ngrp;
   const int tid = threadIdx.x;
   const int64_t npairs = a.NS0 * a.NS1;
@@ -587,13 +588,11 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
     }
     if (mir) {
       // (SYMX runs whole-matrix ranges only: every mirrored row is in range)
-      const int64_t* rpz = a.pat.rp[L];
-      const int64_t* clz = a.pat.cl[L];
       if (m2 >= 2 * (P - 1) && m2 + 2 * P - 1 <= N2) {
         // every row n2 within P-1 of m2 is an interior z row (width W, first
         // column n2 - (P-1), row starts W apart): the mirror offsets are affine in k
         const int64_t ww = w0n * w1n;
-        const int64_t rz = rpz[P - 1] + (m2 - 2 * (P - 1)) * W;  // row start of n2 = m2 - (P-1)
+        const int64_t rz = zrt[3 * (P - 1)] + (m2 - 2 * (P - 1)) * W;  // row start of n2 = m2 - (P-1)
         double* vm = a.values + ((rp0n * w1n + P0 * rp1n) * W + P0 * P1 * rz - base + 2 * (P - 1) * ww +
                                  r1n * w0n + r0n);
         const int64_t step = P0 * P1 * W - ww;
@@ -604,7 +603,7 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
       for (int k = 0; k < W; ++k) {
         const int64_t n2 = m2 + k - (P - 1);
         if (n2 < 0 || n2 >= N2) continue;
-        const int64_t rp2n = rpz[n2], w2n = rpz[n2 + 1] - rp2n, lo2n = clz[rp2n];
+        const int64_t rp2n = zrt[3 * n2], w2n = zrt[3 * n2 + 1], lo2n = zrt[3 * n2 + 2];
         const int64_t startn = rp0n * w1n * w2n + P0 * rp1n * w2n + P0 * P1 * rp2n - base;
         a.values[startn + (m2 - lo2n) * w0n * w1n + r1n * w0n + r0n] = row[k];
       }
@@ -622,6 +621,17 @@ __global__ void __launch_bounds__(NT3, P <= 4 ? 3 : 1) asm_sweep(const Asm3bArgs
   };
   if (tid < NS3) dev::mbar_init(bars + tid, 1);
   dev::fence_mbar_init();
+  if constexpr (SYMX) {
+    // z-row table of the mirrored rows: [row start, width, first column]
+    const int64_t* rpz = a.pat.rp[L];
+    const int64_t* clz = a.pat.cl[L];
+    for (int64_t r = tid; r < N2; r += NT3) {
+      const int64_t rs = rpz[r];
+      zrt[3 * r] = rs;
+      zrt[3 * r + 1] = rpz[r + 1] - rs;
+      zrt[3 * r + 2] = clz[rs];
+    }
+  }
   __syncthreads();
   if (tid == 0)
     for (int e = 0; e < D3; ++e) issue(e_lo + e);
@@ -1611,7 +1621,7 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   if (tile == 0 && !tp.on) return fail(IGS_ECAPACITY, "fused assembly tile does not fit shared memory");
   // A = Aᵀ (whole matrix, whole-grid planes): only the x-pairs n0 >= m0 go
   // through the passes; the z sweep writes each value and its mirror
-  const bool sym_whole = problem_symmetric(p) && !(p->slab_lo || p->slab_hi) && row_lo == 0 &&
+  const bool sym_whole = problem_symmetric(p) && !(p->slab_lo || p->slab_hi) && row_lo == 0 && s.fs.nfn[2] <= 4096 &&
                          row_hi == s.fs.nfn[0] * s.fs.nfn[1] * s.fs.nfn[2];
   // p = 3: the symmetric three-pass path beats the stage-1/2 kernel (0.83 vs
   // 1.02 ms at 64^3 M+K; its 5-wide band wastes the 8-wide MMA tiles of both
@@ -1667,10 +1677,11 @@ igs_status launch3(const igs_problem* p, const AsmShape& s, TensorPat pat, int64
   constexpr size_t smem3 = S3Cfg<P, Q>::SMEM;
   if constexpr (P >= 3) {
     if (symx) {
+      const size_t smem3s = smem3 + 3 * (size_t)s.fs.nfn[2] * sizeof(int64_t);  // + z-row table
       IGS_TRY(cuda_check(cudaFuncSetAttribute(asm_sweep<P, Q, 3, true>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3),
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3s),
                          "smem attribute"));
-      asm_sweep<P, Q, 3, true><<<(unsigned)nbsp, NT3, smem3, st>>>(b);
+      asm_sweep<P, Q, 3, true><<<(unsigned)nbsp, NT3, smem3s, st>>>(b);
       IGS_LAUNCH_CHECK("asm_sweep<3, sym>");
       return IGS_OK;
     }
