@@ -884,15 +884,42 @@ constexpr int forced_zchunks() { return 0; }
 template <bool MASS, bool STIFF>
 bool pick(int P, int Q, Launch* L) {
   if (P != Q) return false;
+#ifdef IGS_DEV_SWITCHES
+  // tile-shape experiments at low orders (measurement builds only)
+  if (apply_variant() >= 10) {
+    switch (apply_variant() * 10 + P) {
+      case 102: *L = make_launch<2, 2, 8, 12, 2, MASS, STIFF, 1>(); return true;
+      case 112: *L = make_launch<2, 2, 8, 12, 1, MASS, STIFF, 2>(); return true;
+      case 122: *L = make_launch<2, 2, 8, 8, 2, MASS, STIFF, 1>(); return true;
+      case 132: *L = make_launch<2, 2, 8, 12, 2, MASS, STIFF, 3>(); return true;
+      case 103: *L = make_launch<3, 3, 8, 8, 1, MASS, STIFF, 1>(); return true;
+      case 113: *L = make_launch<3, 3, 8, 8, 1, MASS, STIFF, 2>(); return true;
+      case 123: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF, 2>(); return true;
+      case 104: *L = make_launch<4, 4, 8, 8, 2, MASS, STIFF, 2>(); return true;
+      case 114: *L = make_launch<4, 4, 8, 8, 2, MASS, STIFF, 1>(); return true;
+      case 124: *L = make_launch<4, 4, 8, 8, 4, MASS, STIFF, 1>(); return true;
+      case 105: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF, 1>(); return true;
+      case 115: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF, 3>(); return true;
+      default: break;
+    }
+  }
+#endif
   switch (P) {
     // p = 4: 8-row y tiles (16 warps) where they fit shared memory (measured
     // 1.51 -> 1.21 ms at 128^3, stiffness), else 4-row tiles (mass+stiffness)
     case 2: *L = make_launch<2, 2, 8, 12, 2, MASS, STIFF>(); return true;
     // p = 3: a single TMA stage lets two CTAs share an SM (18 warps):
     // 0.73 -> 0.66 ms at 128^3 (stiffness)
-    case 3: *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF, 1>(); return true;
+    case 3:  // (mass+stiffness: one point layer per batch on two stages, 0.780 -> 0.764 ms)
+      if (MASS && STIFF) *L = make_launch<3, 3, 8, 8, 1, MASS, STIFF, 2>();
+      else *L = make_launch<3, 3, 8, 8, 3, MASS, STIFF, 1>();
+      return true;
+    // mass+stiffness (7 planes): 8-row tiles fit with two point layers per
+    // batch and a single TMA stage (1.61 -> 1.26 ms at 128^3, 0.72 -> 0.92 of
+    // the copy roofline; the 4-row-tile fallback stays for larger plane sets)
     case 4:
-      *L = make_launch<4, 4, 8, 8, 4, MASS, STIFF>();
+      if (MASS && STIFF) *L = make_launch<4, 4, 8, 8, 2, MASS, STIFF, 1>();
+      else *L = make_launch<4, 4, 8, 8, 4, MASS, STIFF>();
       if (L->smem > 232448) *L = make_launch<4, 4, 8, 4, 4, MASS, STIFF>();
       return true;
     case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
