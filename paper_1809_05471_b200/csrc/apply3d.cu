@@ -902,6 +902,31 @@ bool pick(int P, int Q, Launch* L) {
       case 115: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF, 3>(); return true;
       default: break;
     }
+    // the headline configurations: C4 (p = 6 stiffness), C5 (p = 8 mass+stiffness)
+    if constexpr (!MASS && STIFF) {
+      switch (apply_variant() * 10 + P) {
+        case 206: *L = make_launch<6, 6, 8, 8, 1, MASS, STIFF, 3>(); return true;
+        case 216: *L = make_launch<6, 6, 8, 8, 1, MASS, STIFF, 4>(); return true;
+        case 226: *L = make_launch<6, 6, 8, 8, 3, MASS, STIFF, 2>(); return true;
+        case 236: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 4>(); return true;
+        case 246: *L = make_launch<6, 6, 8, 8, 3, MASS, STIFF, 3>(); return true;
+        case 256: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>(); return true;
+        case 218: *L = make_launch<8, 8, 8, 8, 2, MASS, STIFF, 1>(); return true;
+        case 228: *L = make_launch<8, 8, 8, 8, 1, MASS, STIFF, 1>(); return true;
+        default: break;
+      }
+    }
+    if constexpr (MASS && STIFF) {
+      switch (apply_variant() * 10 + P) {
+        case 208: *L = make_launch<8, 8, 8, 8, 1, MASS, STIFF, 2>(); return true;
+        case 218: *L = make_launch<8, 8, 8, 8, 2, MASS, STIFF, 1>(); return true;
+        case 228: *L = make_launch<8, 8, 8, 6, 1, MASS, STIFF, 3>(); return true;
+        case 238: *L = make_launch<8, 8, 8, 6, 2, MASS, STIFF, 3>(); return true;
+        case 248: *L = make_launch<8, 8, 8, 6, 4, MASS, STIFF, 1>(); return true;
+        case 258: *L = make_launch<8, 8, 8, 6, 2, MASS, STIFF, 1>(); return true;
+        default: break;
+      }
+    }
   }
 #endif
   switch (P) {
@@ -937,6 +962,10 @@ bool pick(int P, int Q, Launch* L) {
     case 8:
       if (apply_variant() == 1) *L = make_launch<8, 8, 8, 4, 2, MASS, STIFF, 4>();
       else if (apply_variant() == 2) *L = make_launch<8, 8, 8, 2, 2, MASS, STIFF, 2>();
+      // stiffness and mass+stiffness (C5): 8-row tiles on a single TMA stage
+      // (C5 sustained 50 applies 10.41 -> 10.13 ms/step, 0.92 -> 0.94 of the
+      // copy roofline; stiffness 9.03 -> 8.66 ms)
+      else if (STIFF) *L = make_launch<8, 8, 8, 8, 2, MASS, STIFF, 1>();
       else *L = make_launch<8, 8, 8, 6, 2, MASS, STIFF, 2>();
       return true;
     default: return false;
