@@ -911,6 +911,12 @@ bool pick(int P, int Q, Launch* L) {
         case 236: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 4>(); return true;
         case 246: *L = make_launch<6, 6, 8, 8, 3, MASS, STIFF, 3>(); return true;
         case 256: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>(); return true;
+        case 306: *L = make_launch<6, 6, 8, 4, 2, MASS, STIFF, 4>(); return true;
+        case 316: *L = make_launch<6, 6, 8, 4, 3, MASS, STIFF, 3>(); return true;
+        case 326: *L = make_launch<6, 6, 8, 4, 6, MASS, STIFF, 2>(); return true;
+        case 336: *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 1>(); return true;
+        case 346: *L = make_launch<6, 6, 8, 4, 6, MASS, STIFF, 1>(); return true;
+        case 356: *L = make_launch<6, 6, 8, 4, 3, MASS, STIFF, 2>(); return true;
         case 218: *L = make_launch<8, 8, 8, 8, 2, MASS, STIFF, 1>(); return true;
         case 228: *L = make_launch<8, 8, 8, 8, 1, MASS, STIFF, 1>(); return true;
         default: break;
