@@ -834,12 +834,13 @@ struct Launch {
   int EX, EY, NT, NPL, QE;
   size_t smem;
   void (*kernel)(ApplyArgs, CUtensorMap);
+  int promo = 256;  // L2 promotion of the coefficient boxes (bytes)
 };
 
 template <int P, int Q, int EX, int EY, int Q2B, bool MASS, bool STIFF, int STG = 2>
 Launch make_launch() {
   using C = Cfg<P, Q, EX, EY, Q2B, MASS, STIFF, STG>;
-  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG>};
+  return Launch{EX, EY, C::NT, C::NPL, C::QE, C::SMEM, &apply3d_kernel<P, Q, EX, EY, Q2B, MASS, STIFF, STG>, 256};
 }
 
 // Development switches, compiled only into the measurement build
@@ -956,7 +957,13 @@ bool pick(int P, int Q, Launch* L) {
     case 5: *L = make_launch<5, 5, 8, 8, 1, MASS, STIFF>(); return true;
     case 6:  // 7 planes (M+K) fit a 2-stage ring, 6 a 3-stage one
       if (apply_variant() == 1 || (MASS && STIFF)) *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 2>();
-      else *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
+      else {
+        // the 3-stage ring hides the box latency itself: 256-byte promotion
+        // only over-fetches there (ncu: 24.7 GB read for 21.8 GB of planes);
+        // 128 bytes: 3.70 -> 3.47 ms at C4, DRAM back to B_alg
+        *L = make_launch<6, 6, 8, 8, 2, MASS, STIFF, 3>();
+        L->promo = 128;
+      }
       return true;
     // p = 7: stiffness on a single TMA stage (two CTAs per SM: 7.35 ->
     // 6.45 ms at 128^3), mass+stiffness on three (8.0 -> 7.7 ms)
@@ -1060,7 +1067,13 @@ Tiling tiling(const FusedShape& s, const Launch& L) {
 // L2 promotion of the coefficient boxes: 64-byte box rows (one 8-point
 // window) gain from 256-byte promotion (the warp's next windows arrive with
 // them: C5 -3 %).
-CUtensorMapL2promotion l2_promotion(const Launch&) { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
+#ifdef IGS_L2_PROMO  // measurement builds: one promotion for every configuration
+CUtensorMapL2promotion l2_promotion(const Launch&) { return IGS_L2_PROMO; }
+#else
+CUtensorMapL2promotion l2_promotion(const Launch& L) {
+  return L.promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+#endif
 
 // The coefficient planes as one 4D tensor (x, y, z points, plane) for TMA.
 // cuTensorMapEncodeTiled comes from the driver through the runtime's entry
