@@ -146,6 +146,11 @@ extern "C" igs_status igs_layers_copy(const double* src, double* dst, int64_t co
 
 namespace igs {
 
+// L2 promotion of the assembly kernels' coefficient boxes (measurement
+// builds override it; 256 bytes measured best or equal everywhere)
+#ifndef IGS_ASM_L2_PROMO
+#define IGS_ASM_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 igs_status planes_tensor_map(CUtensorMap* map, const double* planes, const int64_t dims[4],
                              int64_t pstride, const unsigned box[4]) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -163,7 +168,7 @@ igs_status planes_tensor_map(CUtensorMap* map, const double* planes, const int64
   cuuint32_t es[4] = {1u, 1u, 1u, 1u};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(planes), gd, gs, bd, es,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      IGS_ASM_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(IGS_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return IGS_OK;
 }
