@@ -49,9 +49,10 @@ def apply_row(p, kind, K=128, reps=10):
     torch.cuda.empty_cache()
 
 
-def asm_row(p, kind, K=64, reps=5):
+def asm_row(p, kind, K=64, reps=10):
     prob = workloads.make_problem(3, p, K, kind, max_nnz=1 << 40)
-    A = sumfac.assemble(prob)
+    for _ in range(3):  # warm: allocator, launch data, clocks
+        A = sumfac.assemble(prob)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -67,9 +68,10 @@ def asm_row(p, kind, K=64, reps=5):
     torch.cuda.empty_cache()
 
 
-def asm2_row(p, kind, K=256, reps=10):
+def asm2_row(p, kind, K=256, reps=20):
     prob = workloads.make_problem(2, p, K, kind, max_nnz=1 << 40)
-    A = sumfac.assemble(prob)
+    for _ in range(3):
+        A = sumfac.assemble(prob)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
