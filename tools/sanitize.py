@@ -16,7 +16,6 @@ from paper_1809_05471_b200.bspline import UnivariateBasis, uniform_open_knots  #
 from paper_1809_05471_b200.quadrature import TensorQuadrature, per_element_rule  # noqa: E402
 
 TWO_PASS, GENERIC = 8, 1
-what = sys.argv[1] if len(sys.argv) > 1 else "all"
 
 
 def problem(p, K, kind, seed):
@@ -31,28 +30,30 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-if what in ("apply", "all"):
-    for p, K, kind in [(2, (9, 5, 4), 3), (3, (6, 4, 5), 2), (4, (5, 9, 3), 3), (5, (4, 3, 5), 2),
-                       (6, (6, 5, 4), 2), (7, (3, 4, 3), 3), (8, (3, 4, 3), 3), (8, (2, 3, 4), 2)]:
-        prob = problem(p, K, kind, seed=p)
-        op = matfree.MatrixFreeOperator(prob)
-        x = np.random.default_rng(p).standard_normal(prob.shape[1])
-        y = matfree.apply(op, x)
-        yg = matfree.apply(matfree.MatrixFreeOperator(prob, force_generic=True), x)
-        torch.cuda.synchronize()
-        e = rel(y, yg)
-        print(f"apply p={p} K={K} kind={kind} fused={op.fused} fused-vs-generic {e:.2e}", flush=True)
-        assert e < 1e-12
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("apply", "all"):
+        for p, K, kind in [(2, (9, 5, 4), 3), (3, (6, 4, 5), 2), (4, (5, 9, 3), 3), (5, (4, 3, 5), 2),
+                           (6, (6, 5, 4), 2), (7, (3, 4, 3), 3), (8, (3, 4, 3), 3), (8, (2, 3, 4), 2)]:
+            prob = problem(p, K, kind, seed=p)
+            op = matfree.MatrixFreeOperator(prob)
+            x = np.random.default_rng(p).standard_normal(prob.shape[1])
+            y = matfree.apply(op, x)
+            yg = matfree.apply(matfree.MatrixFreeOperator(prob, force_generic=True), x)
+            torch.cuda.synchronize()
+            e = rel(y, yg)
+            print(f"apply p={p} K={K} kind={kind} fused={op.fused} fused-vs-generic {e:.2e}", flush=True)
+            assert e < 1e-12
 
-if what in ("asm", "all"):
-    for p, K, kind in [(4, (5, 4, 6), 3), (2, (9, 6, 3), 2), (3, (4, 5, 3), 3), (5, (3, 4, 2), 2), (6, (2, 2, 3), 3),
-                       (5, (20, 7), 3), (4, (24, 13), 2), (3, (34, 9), 3), (2, (48, 10), 1)]:
-        prob = problem(p, K, kind, seed=10 + p)
-        A = sumfac.assemble(prob).values_np()
-        A2 = sumfac.assemble(prob, flags=TWO_PASS).values_np()
-        Ag = sumfac.assemble(prob, flags=GENERIC).values_np()
-        torch.cuda.synchronize()
-        e2, eg = rel(A, A2), rel(A, Ag)
-        print(f"asm p={p} K={K} kind={kind} path={sumfac.fused_path(prob)} vs two-pass {e2:.2e} vs generic {eg:.2e}", flush=True)
-        assert e2 < 1e-12 and eg < 1e-12
-print("sanitize cases ok")
+    if what in ("asm", "all"):
+        for p, K, kind in [(4, (5, 4, 6), 3), (2, (9, 6, 3), 2), (3, (4, 5, 3), 3), (5, (3, 4, 2), 2), (6, (2, 2, 3), 3),
+                           (5, (20, 7), 3), (4, (24, 13), 2), (3, (34, 9), 3), (2, (48, 10), 1)]:
+            prob = problem(p, K, kind, seed=10 + p)
+            A = sumfac.assemble(prob).values_np()
+            A2 = sumfac.assemble(prob, flags=TWO_PASS).values_np()
+            Ag = sumfac.assemble(prob, flags=GENERIC).values_np()
+            torch.cuda.synchronize()
+            e2, eg = rel(A, A2), rel(A, Ag)
+            print(f"asm p={p} K={K} kind={kind} path={sumfac.fused_path(prob)} vs two-pass {e2:.2e} vs generic {eg:.2e}", flush=True)
+            assert e2 < 1e-12 and eg < 1e-12
+    print("sanitize cases ok")
