@@ -1324,7 +1324,9 @@ int three_pass_tile(int nplanes) {
   if (AXCfg<P, P, 6>::smem(nplanes) <= 232448) return 6;
   if (AXCfg<P, P, 4>::smem(nplanes) <= 232448) return 4;
   if (AXCfg<P, P, 2>::smem(nplanes) <= 232448) return 2;
-  if (AXCfg<P, P, 1>::smem(nplanes) <= 232448) return 1;
+  // (a 1-row tile starts its TMA box at x point (t - P + 1)·P: odd, i.e. not
+  // 16-byte aligned, for odd p and odd t)
+  if (P % 2 == 0 && AXCfg<P, P, 1>::smem(nplanes) <= 232448) return 1;
   return 0;
 }
 
